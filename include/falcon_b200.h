@@ -1,0 +1,195 @@
+/*
+ * falcon_b200.h -- C ABI of the B200-native Falcon codec (libfalcon_b200.so).
+ *
+ * Plain pointers and sizes only; no torch or C++ types cross this boundary.  Every
+ * entry point replaces one reference interface (paths under /root/reference/proj):
+ *
+ *   falcon_compress_stream    <- falcon::compress_pipeline<T>(value_source<T>&,
+ *                                   const pipeline_options&, pipeline_stats*)
+ *                                   include/falcon/pipeline.hpp:156-159
+ *   falcon_decompress_stream  <- falcon::decompress_pipeline<T>(span<const u8>,
+ *                                   value_sink<T>&, const pipeline_options&)
+ *                                   include/falcon/pipeline.hpp:370-373
+ *   falcon_decompress_host    <- falcon::decompress_to_vector<T> (pipeline.hpp:469-476)
+ *   falcon_compress_host      <- compress_pipeline over a memory_source (pipeline.hpp:37-52)
+ *   falcon_compress_device    <- (new) device-resident form of compress_pipeline
+ *   falcon_decompress_device  <- (new) device-resident form of decompress_pipeline
+ *   falcon_compress_chunk     <- falcon::compress_chunk<T>   chunk_codec.hpp:50-82
+ *   falcon_decompress_chunk   <- falcon::decompress_chunk<T> chunk_codec.hpp:86-131
+ *   falcon_max_encoded_chunk_size <- max_encoded_chunk_size<T> chunk_codec.hpp:36-41
+ *   falcon_write_header / falcon_read_header <- write_header / read_header
+ *                                   src/container.cpp:44-86
+ *   falcon_synth_fill         <- synth::generator<T>::fill   include/falcon/synthetic.hpp:36-115
+ *
+ * Errors: every call returns a falcon_status; the message of the last failure on the
+ * calling thread is falcon_last_error().  The status maps onto the reference's
+ * exception types (error.hpp:8-19): FALCON_ERR_INVALID -> falcon::error,
+ * FALCON_ERR_CORRUPT -> falcon::corrupt_error, FALCON_ERR_IO -> falcon::io_error.
+ * Messages are the reference's own texts, including the " (batch N)" suffix.
+ *
+ * Output bytes never depend on n_streams, workers or the GPU count (FORMAT.md:3-6).
+ */
+#ifndef FALCON_B200_H
+#define FALCON_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FALCON_B200_ABI_VERSION 1
+
+typedef enum {
+    FALCON_OK = 0,
+    FALCON_ERR_INVALID = 1,     /* falcon::error: bad options, precision mismatch, ... */
+    FALCON_ERR_CORRUPT = 2,     /* falcon::corrupt_error: malformed archive bytes */
+    FALCON_ERR_IO = 3,          /* falcon::io_error */
+    FALCON_ERR_CUDA = 4,        /* CUDA runtime failure (message has the CUDA error) */
+    FALCON_ERR_CALLBACK = 5,    /* a source/sink callback reported failure */
+    FALCON_ERR_CAPACITY = 6,    /* caller-provided output buffer too small */
+    FALCON_ERR_UNSUPPORTED = 7  /* valid but not supported by this build (chunk_n > 8193) */
+} falcon_status;
+
+typedef enum { FALCON_F64 = 0, FALCON_F32 = 1 } falcon_precision;  /* container.hpp:15 tag */
+
+/* Pipeline stage ids for the stage_delay test hook (pipeline.hpp:66-68). */
+#define FALCON_STAGE_COMPRESS 0
+#define FALCON_STAGE_STORE 1
+#define FALCON_STAGE_DECODE 2
+
+/* pipeline_options (pipeline.hpp:70-79). */
+typedef struct {
+    uint32_t chunk_n;        /* values per chunk, 64k+1 (default 1025) */
+    uint64_t batch_values;   /* values per batch (default 1025*1024*4) */
+    uint32_t n_streams;      /* batches in flight (default 16) */
+    uint32_t workers;        /* host threads for source/sink work (0 = FALCON_WORKERS / hw) */
+    /* optional: runs right before a stage's completion is signalled (test hook) */
+    void (*stage_delay)(void* user, int stage, unsigned slot, uint64_t seq);
+    void* stage_delay_user;
+} falcon_pipeline_options;
+
+/* pipeline_stats (pipeline.hpp:81-85). */
+typedef struct {
+    uint64_t batches;
+    uint64_t values;
+    uint64_t blocking_waits;
+} falcon_pipeline_stats;
+
+/* archive_header (container.hpp:12-27). */
+typedef struct {
+    uint8_t precision;
+    uint32_t chunk_n;
+    uint64_t batch_values;
+    uint64_t total_values;
+    uint64_t batch_count;
+} falcon_archive_info;
+
+typedef struct falcon_ctx falcon_ctx;
+
+/* value_source<T>::read (pipeline.hpp:21-27): fill up to max_values values at dst and
+ * return how many were written; 0 = end of stream; < 0 = failure (the call then fails
+ * with FALCON_ERR_CALLBACK after in-flight work drains). */
+typedef int64_t (*falcon_read_fn)(void* user, void* dst, uint64_t max_values);
+/* Archive writer used by falcon_compress_stream: called once per batch frame, in launch
+ * order, with the frame's final archive offset; plus once with offset 0 for the 47-byte
+ * header at the end.  Nonzero return = failure. */
+typedef int (*falcon_store_fn)(void* user, uint64_t offset, const void* bytes, uint64_t len);
+/* value_sink<T>::put (pipeline.hpp:29-35): one call per batch, possibly out of order and
+ * from several host threads; the span is only valid during the call.  Nonzero = failure. */
+typedef int (*falcon_put_fn)(void* user, uint64_t first_value, const void* values, uint64_t count);
+
+/* ---- library / context ---- */
+int falcon_abi_version(void);
+const char* falcon_last_error(void);
+void falcon_default_options(falcon_pipeline_options* opt);
+falcon_status falcon_ctx_create(int device, falcon_ctx** out);
+void falcon_ctx_destroy(falcon_ctx* ctx);
+
+/* ---- format helpers (host only, no GPU) ---- */
+uint64_t falcon_max_encoded_chunk_size(int precision, uint32_t chunk_n);
+/* Worst-case archive size: 47 + sum_b (4 + 4*C_b + C_b * max_encoded_chunk_size). */
+uint64_t falcon_compress_bound(int precision, uint64_t n_values, uint32_t chunk_n,
+                               uint64_t batch_values);
+void falcon_write_header(const falcon_archive_info* info, uint8_t out[47]);
+falcon_status falcon_read_header(const uint8_t* bytes, uint64_t len, falcon_archive_info* out);
+
+/* ---- device-resident (all pointers are device pointers on ctx's GPU) ---- */
+/* Compress n_values values at d_values into d_out (capacity out_cap >= bound).  The
+ * archive length is returned in *out_bytes (host); the call synchronises `stream`. */
+falcon_status falcon_compress_device(falcon_ctx* ctx, int precision, const void* d_values,
+                                     uint64_t n_values, uint32_t chunk_n, uint64_t batch_values,
+                                     void* d_out, uint64_t out_cap, uint64_t* out_bytes,
+                                     void* stream);
+/* Asynchronous form: enqueues the work on `stream` and returns.  The archive length is
+ * written to d_out_bytes (device u64).  Errors surface in falcon_ctx_sync(). */
+falcon_status falcon_compress_device_async(falcon_ctx* ctx, int precision, const void* d_values,
+                                           uint64_t n_values, uint32_t chunk_n,
+                                           uint64_t batch_values, void* d_out, uint64_t out_cap,
+                                           uint64_t* d_out_bytes, void* stream);
+/* Decompress the archive at d_archive (archive_bytes long) into d_values (cap_values).
+ * Reads the header back to the host first; synchronises `stream`. */
+falcon_status falcon_decompress_device(falcon_ctx* ctx, int precision, const void* d_archive,
+                                       uint64_t archive_bytes, void* d_values,
+                                       uint64_t cap_values, uint64_t* n_values, void* stream);
+/* Asynchronous form for a caller that already holds the parsed header. */
+falcon_status falcon_decompress_device_async(falcon_ctx* ctx, int precision,
+                                             const void* d_archive, uint64_t archive_bytes,
+                                             const falcon_archive_info* info, void* d_values,
+                                             uint64_t cap_values, void* stream);
+/* Wait for `stream` and report the first error raised by async calls on ctx. */
+falcon_status falcon_ctx_sync(falcon_ctx* ctx, void* stream);
+
+/* ---- host-resident: multi-stream pinned H2D / kernel / D2H pipeline ---- */
+falcon_status falcon_compress_stream(falcon_ctx* ctx, int precision, falcon_read_fn read,
+                                     void* read_user, falcon_store_fn store, void* store_user,
+                                     const falcon_pipeline_options* opt,
+                                     falcon_pipeline_stats* stats);
+falcon_status falcon_decompress_stream(falcon_ctx* ctx, int precision, const uint8_t* archive,
+                                       uint64_t archive_bytes, falcon_put_fn put, void* put_user,
+                                       const falcon_pipeline_options* opt,
+                                       falcon_pipeline_stats* stats);
+/* Convenience: host buffers in, host buffers out. */
+falcon_status falcon_compress_host(falcon_ctx* ctx, int precision, const void* values,
+                                   uint64_t n_values, const falcon_pipeline_options* opt,
+                                   uint8_t* out, uint64_t out_cap, uint64_t* out_bytes,
+                                   falcon_pipeline_stats* stats);
+falcon_status falcon_decompress_host(falcon_ctx* ctx, int precision, const uint8_t* archive,
+                                     uint64_t archive_bytes, void* values, uint64_t cap_values,
+                                     uint64_t* n_values, const falcon_pipeline_options* opt,
+                                     falcon_pipeline_stats* stats);
+
+/* ---- per-chunk operators (GPU-backed; host buffers) ---- */
+/* Encodes exactly chunk_n values; returns the encoded length in *out_len. */
+falcon_status falcon_compress_chunk(falcon_ctx* ctx, int precision, const void* values,
+                                    uint32_t chunk_n, uint8_t* out, uint64_t out_cap,
+                                    uint64_t* out_len);
+/* Decodes one encoded chunk of `len` bytes; emits `count` (<= chunk_n) values. */
+falcon_status falcon_decompress_chunk(falcon_ctx* ctx, int precision, const uint8_t* in,
+                                      uint64_t len, uint32_t chunk_n, uint32_t count,
+                                      void* values);
+
+/* ---- synthetic inputs (synthetic.hpp:14-32 kinds; kind 5 = the pinned cfg3 kind) ---- */
+#define FALCON_KIND_WALK 0
+#define FALCON_KIND_DECIMAL 1
+#define FALCON_KIND_SIGNFLIP 2
+#define FALCON_KIND_OUTLIER 3
+#define FALCON_KIND_BITS 4
+#define FALCON_KIND_MIXED_BLOCKS 5
+typedef struct {
+    int kind;
+    int decimal_places;
+    uint64_t seed;
+    int max_step_units;
+    uint64_t outlier_period;
+    int64_t outlier_units;
+    uint32_t block;     /* MIXED_BLOCKS: values per decimal-place block (chunk_n) */
+} falcon_synth_spec;
+falcon_status falcon_synth_fill(int precision, const falcon_synth_spec* spec, void* out,
+                                uint64_t count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FALCON_B200_H */

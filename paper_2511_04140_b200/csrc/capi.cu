@@ -1,0 +1,477 @@
+// capi.cu -- C ABI: library/context, format helpers, device-resident compress and
+// decompress, per-chunk operators, synthetic inputs.  The host-resident multi-stream
+// pipeline lives in pipeline.cu.
+#include <mutex>
+#include <random>
+
+#include "runtime.h"
+
+namespace fb200 {
+const char* last_error_text();
+}
+
+using namespace fb200;
+
+namespace {
+
+struct device_guard {
+    int prev = -1;
+    explicit device_guard(int d) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != d) cudaSetDevice(d);
+    }
+    ~device_guard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+std::once_flag g_table_once[64];
+cudaError_t g_table_err[64];
+
+// misc scratch layout (ctx->misc, device)
+constexpr size_t kEncTicket = 0, kEncError = 8, kEncTotal = 16, kDecTicket = 24, kDecAbort = 32,
+                 kDecError = 40, kMiscBytes = 64;
+
+uint8_t* misc_at(falcon_ctx* ctx, size_t off) { return ctx->misc.as<uint8_t>() + off; }
+
+falcon_status error_from_device(unsigned long long word, uint64_t cpb, bool batch_suffix) {
+    if (word == ~0ull) return FALCON_OK;
+    const uint32_t code = (uint32_t)(word & 0xff);
+    const uint64_t key = word >> 8;
+    std::string msg = device_error_text(code);
+    if (batch_suffix && code != DEV_E_TRAILING && code != DEV_E_CAPACITY && code != DEV_E_SCALE)
+        msg += " (batch " + std::to_string(key / cpb) + ")";
+    return set_error(device_error_status(code), msg);
+}
+
+encode_ws ctx_encode_ws(falcon_ctx* ctx, uint64_t* d_total) {
+    encode_ws ws;
+    ws.status = ctx->enc_status.as<uint64_t>();
+    ws.ticket = reinterpret_cast<uint32_t*>(misc_at(ctx, kEncTicket));
+    ws.error = reinterpret_cast<unsigned long long*>(misc_at(ctx, kEncError));
+    ws.total = d_total ? d_total : reinterpret_cast<uint64_t*>(misc_at(ctx, kEncTotal));
+    return ws;
+}
+
+decode_ws ctx_decode_ws(falcon_ctx* ctx) {
+    decode_ws ws;
+    ws.ticket = reinterpret_cast<uint32_t*>(misc_at(ctx, kDecTicket));
+    ws.ready = ctx->dec_ready.as<uint32_t>();
+    ws.abort_at = reinterpret_cast<unsigned long long*>(misc_at(ctx, kDecAbort));
+    ws.chunk_off = ctx->dec_off.as<uint64_t>();
+    ws.chunk_size = ctx->dec_size.as<uint32_t>();
+    ws.error = reinterpret_cast<unsigned long long*>(misc_at(ctx, kDecError));
+    return ws;
+}
+
+falcon_status enqueue_compress(falcon_ctx* ctx, int prec, const void* d_values, uint64_t n,
+                               uint32_t chunk_n, uint64_t bv, void* d_out, uint64_t cap,
+                               uint64_t* d_total, cudaStream_t st, geometry& g) {
+    FB_TRY(validate_options(chunk_n, bv));
+    FB_TRY(make_geometry(n, chunk_n, bv, 47, g));
+    FB_TRY(ctx->enc_status.ensure(g.n_chunks * sizeof(uint64_t) + 8));
+    const archive_header_bytes hdr = header_bytes_of(prec, chunk_n, bv, n, g.n_batches);
+    if (cap < 47) return set_error(FALCON_ERR_CAPACITY, "output capacity too small for the header");
+    const encode_ws ws = ctx_encode_ws(ctx, d_total);
+    cudaError_t e = prec == FALCON_F64
+                        ? launch_encode<double>(static_cast<const double*>(d_values), g,
+                                                static_cast<uint8_t*>(d_out), cap, ws, hdr, st)
+                        : launch_encode<float>(static_cast<const float*>(d_values), g,
+                                               static_cast<uint8_t*>(d_out), cap, ws, hdr, st);
+    if (e != cudaSuccess) return set_error(FALCON_ERR_CUDA, std::string("encode launch: ") + cudaGetErrorString(e));
+    return FALCON_OK;
+}
+
+falcon_status parse_header(const uint8_t* in, uint64_t len, falcon_archive_info* h) {
+    // read_header (container.cpp:57-86)
+    static const uint8_t magic[8] = {'F', 'A', 'L', 'C', 'O', 'N', 'A', 0};
+    auto get = [&](int off, int bytes) {
+        uint64_t v = 0;
+        for (int i = 0; i < bytes; ++i) v |= (uint64_t)in[off + i] << (8 * i);
+        return v;
+    };
+    if (len < 47) return set_error(FALCON_ERR_CORRUPT, "archive header truncated");
+    if (std::memcmp(in, magic, 8) != 0) return set_error(FALCON_ERR_CORRUPT, "bad archive magic");
+    if (get(8, 2) != 1) return set_error(FALCON_ERR_CORRUPT, "unsupported archive version");
+    if (in[10] > 1) return set_error(FALCON_ERR_CORRUPT, "unknown precision tag");
+    h->precision = in[10];
+    h->chunk_n = (uint32_t)get(11, 4);
+    if (h->chunk_n < 65 || (h->chunk_n - 1) % 64 != 0)
+        return set_error(FALCON_ERR_CORRUPT, "invalid chunk length");
+    h->batch_values = get(15, 8);
+    h->total_values = get(23, 8);
+    h->batch_count = get(31, 8);
+    if (h->batch_values == 0 && h->total_values != 0)
+        return set_error(FALCON_ERR_CORRUPT, "zero batch size with nonzero value count");
+    if (h->batch_values != 0) {
+        const uint64_t expect = (h->total_values + h->batch_values - 1) / h->batch_values;
+        if (expect != h->batch_count)
+            return set_error(FALCON_ERR_CORRUPT, "batch count disagrees with value count");
+    } else if (h->batch_count != 0) {
+        return set_error(FALCON_ERR_CORRUPT, "batch count disagrees with value count");
+    }
+    return FALCON_OK;
+}
+
+falcon_status enqueue_decompress(falcon_ctx* ctx, int prec, const void* d_archive, uint64_t bytes,
+                                 const falcon_archive_info* info, void* d_values, uint64_t cap,
+                                 cudaStream_t st, geometry& g) {
+    if (info->precision != prec)
+        return set_error(FALCON_ERR_INVALID, "archive precision does not match the requested value type");
+    if (info->total_values > cap)
+        return set_error(FALCON_ERR_CAPACITY, "value capacity too small for the archive");
+    if (info->chunk_n > 8193)
+        return set_error(FALCON_ERR_UNSUPPORTED,
+                         "chunk_n > 8193 is not supported by the sm_100a kernels of this build");
+    FB_TRY(make_geometry(info->total_values, info->chunk_n, info->batch_values ? info->batch_values : 1,
+                         47, g));
+    if (g.n_chunks == 0) {
+        if (bytes != 47) return set_error(FALCON_ERR_CORRUPT, "trailing bytes after final batch");
+        return FALCON_OK;
+    }
+    FB_TRY(ctx->dec_off.ensure(g.n_chunks * sizeof(uint64_t)));
+    FB_TRY(ctx->dec_size.ensure(g.n_chunks * sizeof(uint32_t)));
+    FB_TRY(ctx->dec_ready.ensure(g.n_batches * sizeof(uint32_t)));
+    const decode_ws ws = ctx_decode_ws(ctx);
+    cudaError_t e = prec == FALCON_F64
+                        ? launch_decode<double>(static_cast<const uint8_t*>(d_archive), bytes, g,
+                                                static_cast<double*>(d_values), ws, st)
+                        : launch_decode<float>(static_cast<const uint8_t*>(d_archive), bytes, g,
+                                               static_cast<float*>(d_values), ws, st);
+    if (e != cudaSuccess) return set_error(FALCON_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
+    return FALCON_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int falcon_abi_version(void) { return FALCON_B200_ABI_VERSION; }
+
+const char* falcon_last_error(void) { return fb200::last_error_text(); }
+
+void falcon_default_options(falcon_pipeline_options* opt) {
+    // pipeline_options defaults (pipeline.hpp:70-79)
+    opt->chunk_n = 1025;
+    opt->batch_values = 1025ull * 1024 * 4;
+    opt->n_streams = 16;
+    opt->workers = 0;
+    opt->stage_delay = nullptr;
+    opt->stage_delay_user = nullptr;
+}
+
+falcon_status falcon_ctx_create(int device, falcon_ctx** out) {
+    *out = nullptr;
+    int count = 0;
+    FB_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count || device >= 64)
+        return set_error(FALCON_ERR_INVALID, "invalid CUDA device index");
+    device_guard dg(device);
+    std::call_once(g_table_once[device], [device] { g_table_err[device] = upload_tables(); });
+    if (g_table_err[device] != cudaSuccess)
+        return set_error(FALCON_ERR_CUDA, std::string("table upload: ") + cudaGetErrorString(g_table_err[device]));
+    auto ctx = std::make_unique<falcon_ctx>();
+    ctx->device = device;
+    FB_TRY(ctx->misc.ensure(kMiscBytes));
+    FB_CUDA(cudaMemset(ctx->misc.p, 0xff, kMiscBytes));
+    FB_TRY(ctx->host_box.ensure(sizeof(slot_mailbox) * 4));
+    *out = ctx.release();
+    return FALCON_OK;
+}
+
+void falcon_ctx_destroy(falcon_ctx* ctx) {
+    if (!ctx) return;
+    device_guard dg(ctx->device);
+    cudaDeviceSynchronize();
+    delete ctx;
+}
+
+uint64_t falcon_max_encoded_chunk_size(int precision, uint32_t chunk_n) {
+    return max_chunk_bytes(precision, chunk_n);
+}
+
+uint64_t falcon_compress_bound(int precision, uint64_t n_values, uint32_t chunk_n,
+                               uint64_t batch_values) {
+    if (chunk_n < 65 || batch_values == 0) return 0;
+    uint64_t total = 47;
+    const uint64_t batches = (n_values + batch_values - 1) / batch_values;
+    if (batches == 0) return total;
+    total += (batches - 1) * frame_bound(precision, batch_values, chunk_n);
+    total += frame_bound(precision, n_values - (batches - 1) * batch_values, chunk_n);
+    return total;
+}
+
+void falcon_write_header(const falcon_archive_info* info, uint8_t out[47]) {
+    const archive_header_bytes h = header_bytes_of(info->precision, info->chunk_n, info->batch_values,
+                                                   info->total_values, info->batch_count);
+    std::memcpy(out, h.b, 47);
+}
+
+falcon_status falcon_read_header(const uint8_t* bytes, uint64_t len, falcon_archive_info* out) {
+    return parse_header(bytes, len, out);
+}
+
+// ---- device-resident ----------------------------------------------------------
+falcon_status falcon_compress_device_async(falcon_ctx* ctx, int precision, const void* d_values,
+                                           uint64_t n_values, uint32_t chunk_n,
+                                           uint64_t batch_values, void* d_out, uint64_t out_cap,
+                                           uint64_t* d_out_bytes, void* stream) {
+    if (!ctx) return set_error(FALCON_ERR_INVALID, "null context");
+    std::lock_guard<std::mutex> lock(ctx->api_mutex);
+    device_guard dg(ctx->device);
+    geometry g;
+    return enqueue_compress(ctx, precision, d_values, n_values, chunk_n, batch_values, d_out, out_cap,
+                            d_out_bytes, static_cast<cudaStream_t>(stream), g);
+}
+
+falcon_status falcon_compress_device(falcon_ctx* ctx, int precision, const void* d_values,
+                                     uint64_t n_values, uint32_t chunk_n, uint64_t batch_values,
+                                     void* d_out, uint64_t out_cap, uint64_t* out_bytes,
+                                     void* stream) {
+    if (!ctx) return set_error(FALCON_ERR_INVALID, "null context");
+    std::lock_guard<std::mutex> lock(ctx->api_mutex);
+    device_guard dg(ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    FB_CUDA(cudaMemsetAsync(misc_at(ctx, kEncError), 0xff, 8, st));
+    geometry g;
+    FB_TRY(enqueue_compress(ctx, precision, d_values, n_values, chunk_n, batch_values, d_out, out_cap,
+                            nullptr, st, g));
+    slot_mailbox* box = ctx->host_box.as<slot_mailbox>();
+    FB_CUDA(cudaMemcpyAsync(&box->total, misc_at(ctx, kEncTotal), 8, cudaMemcpyDeviceToHost, st));
+    FB_CUDA(cudaMemcpyAsync(&box->error, misc_at(ctx, kEncError), 8, cudaMemcpyDeviceToHost, st));
+    FB_CUDA(cudaStreamSynchronize(st));
+    FB_TRY(error_from_device(box->error, g.cpb, false));
+    if (box->total > out_cap)
+        return set_error(FALCON_ERR_CAPACITY, "output capacity too small for the compressed archive");
+    if (out_bytes) *out_bytes = box->total;
+    return FALCON_OK;
+}
+
+falcon_status falcon_decompress_device_async(falcon_ctx* ctx, int precision,
+                                             const void* d_archive, uint64_t archive_bytes,
+                                             const falcon_archive_info* info, void* d_values,
+                                             uint64_t cap_values, void* stream) {
+    if (!ctx || !info) return set_error(FALCON_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lock(ctx->api_mutex);
+    device_guard dg(ctx->device);
+    geometry g;
+    return enqueue_decompress(ctx, precision, d_archive, archive_bytes, info, d_values, cap_values,
+                              static_cast<cudaStream_t>(stream), g);
+}
+
+falcon_status falcon_decompress_device(falcon_ctx* ctx, int precision, const void* d_archive,
+                                       uint64_t archive_bytes, void* d_values,
+                                       uint64_t cap_values, uint64_t* n_values, void* stream) {
+    if (!ctx) return set_error(FALCON_ERR_INVALID, "null context");
+    std::lock_guard<std::mutex> lock(ctx->api_mutex);
+    device_guard dg(ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint8_t* hb = ctx->host_box.as<uint8_t>();   // reuse pinned mailbox for the header
+    FB_TRY(ctx->host_box.ensure(64));
+    hb = ctx->host_box.as<uint8_t>();
+    const uint64_t hl = archive_bytes < 47 ? archive_bytes : 47;
+    if (hl) FB_CUDA(cudaMemcpyAsync(hb, d_archive, hl, cudaMemcpyDeviceToHost, st));
+    FB_CUDA(cudaStreamSynchronize(st));
+    uint8_t header[47];
+    std::memcpy(header, hb, hl);
+    falcon_archive_info info;
+    FB_TRY(parse_header(header, archive_bytes, &info));
+    FB_CUDA(cudaMemsetAsync(misc_at(ctx, kDecError), 0xff, 8, st));
+    geometry g;
+    FB_TRY(enqueue_decompress(ctx, precision, d_archive, archive_bytes, &info, d_values, cap_values, st, g));
+    unsigned long long err = ~0ull;
+    FB_CUDA(cudaMemcpyAsync(hb, misc_at(ctx, kDecError), 8, cudaMemcpyDeviceToHost, st));
+    FB_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(&err, hb, 8);
+    FB_TRY(error_from_device(err, g.cpb, true));
+    if (n_values) *n_values = info.total_values;
+    return FALCON_OK;
+}
+
+falcon_status falcon_ctx_sync(falcon_ctx* ctx, void* stream) {
+    if (!ctx) return set_error(FALCON_ERR_INVALID, "null context");
+    std::lock_guard<std::mutex> lock(ctx->api_mutex);
+    device_guard dg(ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    unsigned long long errs[2];
+    uint8_t* hb = ctx->host_box.as<uint8_t>();
+    FB_CUDA(cudaMemcpyAsync(hb, misc_at(ctx, kEncError), 8, cudaMemcpyDeviceToHost, st));
+    FB_CUDA(cudaMemcpyAsync(hb + 8, misc_at(ctx, kDecError), 8, cudaMemcpyDeviceToHost, st));
+    FB_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(errs, hb, 16);
+    FB_CUDA(cudaMemsetAsync(misc_at(ctx, kEncError), 0xff, 8, st));
+    FB_CUDA(cudaMemsetAsync(misc_at(ctx, kDecError), 0xff, 8, st));
+    FB_CUDA(cudaStreamSynchronize(st));
+    // batch index of an async error is not recoverable without the geometry; report the text
+    FB_TRY(error_from_device(errs[0], 1, false));
+    FB_TRY(error_from_device(errs[1], 1, false));
+    return FALCON_OK;
+}
+
+// ---- per-chunk operators ---------------------------------------------------------
+falcon_status falcon_compress_chunk(falcon_ctx* ctx, int precision, const void* values,
+                                    uint32_t chunk_n, uint8_t* out, uint64_t out_cap,
+                                    uint64_t* out_len) {
+    if (!ctx) return set_error(FALCON_ERR_INVALID, "null context");
+    FB_TRY(validate_options(chunk_n, chunk_n));
+    const size_t esz = lane_bytes(precision);
+    const uint64_t bound = falcon_compress_bound(precision, chunk_n, chunk_n, chunk_n);
+    device_buffer din, dout;
+    FB_TRY(din.ensure(chunk_n * esz));
+    FB_TRY(dout.ensure(bound));
+    {
+        device_guard dg(ctx->device);
+        FB_CUDA(cudaMemcpy(din.p, values, chunk_n * esz, cudaMemcpyHostToDevice));
+    }
+    uint64_t bytes = 0;
+    FB_TRY(falcon_compress_device(ctx, precision, din.p, chunk_n, chunk_n, chunk_n, dout.p, bound,
+                                  &bytes, nullptr));
+    // archive = 47 header + [u32 1][u32 size] + chunk
+    const uint64_t len = bytes - 47 - 8;
+    if (len > out_cap) return set_error(FALCON_ERR_CAPACITY, "chunk output capacity too small");
+    {
+        device_guard dg(ctx->device);
+        FB_CUDA(cudaMemcpy(out, dout.as<uint8_t>() + 47 + 8, len, cudaMemcpyDeviceToHost));
+    }
+    *out_len = len;
+    return FALCON_OK;
+}
+
+falcon_status falcon_decompress_chunk(falcon_ctx* ctx, int precision, const uint8_t* in,
+                                      uint64_t len, uint32_t chunk_n, uint32_t count, void* values) {
+    if (!ctx) return set_error(FALCON_ERR_INVALID, "null context");
+    if (count > chunk_n)  // chunk_codec.hpp:92-93
+        return set_error(FALCON_ERR_INVALID, "decompress_chunk: count exceeds chunk capacity");
+    if (len > 0xffffffffull) return set_error(FALCON_ERR_CORRUPT, "chunk size mismatch");
+    // wrap the chunk in a one-chunk archive: the device decoder runs the exact
+    // decompress_chunk validation; decode all chunk_n lanes, keep `count`
+    std::vector<uint8_t> arc(47 + 8 + len);
+    const archive_header_bytes h = header_bytes_of(precision, chunk_n, chunk_n, chunk_n, 1);
+    std::memcpy(arc.data(), h.b, 47);
+    const uint32_t one = 1, sz = (uint32_t)len;
+    std::memcpy(arc.data() + 47, &one, 4);
+    std::memcpy(arc.data() + 51, &sz, 4);
+    if (len) std::memcpy(arc.data() + 55, in, len);
+    const size_t esz = lane_bytes(precision);
+    device_buffer darc, dval;
+    FB_TRY(darc.ensure(arc.size()));
+    FB_TRY(dval.ensure(chunk_n * esz));
+    {
+        device_guard dg(ctx->device);
+        FB_CUDA(cudaMemcpy(darc.p, arc.data(), arc.size(), cudaMemcpyHostToDevice));
+    }
+    uint64_t nv = 0;
+    falcon_status s = falcon_decompress_device(ctx, precision, darc.p, arc.size(), dval.p, chunk_n, &nv,
+                                               nullptr);
+    if (s != FALCON_OK) {
+        // strip the synthetic " (batch 0)" suffix: chunk-level calls carry no batch index
+        std::string m = falcon_last_error();
+        const std::string suf = " (batch 0)";
+        if (m.size() > suf.size() && m.compare(m.size() - suf.size(), suf.size(), suf) == 0)
+            m.resize(m.size() - suf.size());
+        return set_error(s, m);
+    }
+    {
+        device_guard dg(ctx->device);
+        if (count) FB_CUDA(cudaMemcpy(values, dval.p, count * esz, cudaMemcpyDeviceToHost));
+    }
+    return FALCON_OK;
+}
+
+// ---- synthetic generators (synthetic.hpp:36-115) ------------------------------------
+falcon_status falcon_synth_fill(int precision, const falcon_synth_spec* s, void* out, uint64_t count) {
+    const int max_alpha = precision == FALCON_F64 ? 22 : 10;
+    const int max_beta = precision == FALCON_F64 ? 15 : 6;
+    if (s->decimal_places < 0 || s->decimal_places > max_alpha)
+        return set_error(FALCON_ERR_INVALID, "decimal_places out of range for this precision");
+    if (s->max_step_units < 1) return set_error(FALCON_ERR_INVALID, "max_step_units must be positive");
+    std::mt19937_64 rng(s->seed);
+    int64_t acc = (int64_t)(rng() % 20001) - 10000;
+    uint64_t next_outlier = 0;
+    if (s->kind == FALCON_KIND_OUTLIER) {
+        if (s->outlier_period == 0) return set_error(FALCON_ERR_INVALID, "outlier_period must be positive");
+        next_outlier = rng() % s->outlier_period;
+    }
+    if (s->kind == FALCON_KIND_MIXED_BLOCKS && s->block == 0)
+        return set_error(FALCON_ERR_INVALID, "mixed-blocks generator needs a block length");
+    double p64[23];
+    float p32[11];
+    {
+        double d = 1;
+        for (int i = 0; i < 23; ++i, d *= 10) p64[i] = d;
+        float f = 1;
+        for (int i = 0; i < 11; ++i, f *= 10) p32[i] = f;
+    }
+    auto emit = [&](uint64_t i, int64_t units, int dp) {
+        if (precision == FALCON_F64) static_cast<double*>(out)[i] = (double)units / p64[dp];
+        else static_cast<float*>(out)[i] = (float)units / p32[dp];
+    };
+    int dp_block = s->decimal_places;
+    for (uint64_t i = 0; i < count; ++i) {
+        switch (s->kind) {
+        case FALCON_KIND_WALK:
+        case FALCON_KIND_OUTLIER: {
+            const int64_t span = 2 * (int64_t)s->max_step_units + 1;
+            acc += (int64_t)(rng() % (uint64_t)span) - s->max_step_units;
+            int64_t units = acc;
+            if (s->kind == FALCON_KIND_OUTLIER && i == next_outlier) {
+                units += s->outlier_units;
+                next_outlier += s->outlier_period;
+            }
+            emit(i, units, s->decimal_places);
+            break;
+        }
+        case FALCON_KIND_DECIMAL: {
+            const int digits = 1 + (int)(rng() % (uint64_t)max_beta);
+            int64_t lo = 1, hi = 10;
+            for (int k = 1; k < digits; ++k) {
+                lo *= 10;
+                hi *= 10;
+            }
+            int64_t d = lo + (int64_t)(rng() % (uint64_t)(hi - lo));
+            if (d % 10 == 0) ++d;
+            if (rng() & 1) d = -d;
+            emit(i, d, s->decimal_places);
+            break;
+        }
+        case FALCON_KIND_SIGNFLIP: {
+            const uint64_t r = rng();
+            if (precision == FALCON_F64) {
+                uint64_t b = (r & ((1ull << 52) - 1)) | (1023ull << 52) | ((i & 1) << 63);
+                std::memcpy(static_cast<double*>(out) + i, &b, 8);
+            } else {
+                uint32_t b = ((uint32_t)r & ((1u << 23) - 1)) | (127u << 23) | ((uint32_t)(i & 1) << 31);
+                std::memcpy(static_cast<float*>(out) + i, &b, 4);
+            }
+            break;
+        }
+        case FALCON_KIND_BITS: {
+            const uint64_t r = rng();
+            if (precision == FALCON_F64) std::memcpy(static_cast<double*>(out) + i, &r, 8);
+            else {
+                const uint32_t b = (uint32_t)r;
+                std::memcpy(static_cast<float*>(out) + i, &b, 4);
+            }
+            break;
+        }
+        case FALCON_KIND_MIXED_BLOCKS: {
+            // pinned cfg3 generator: reflecting walk in +/-999999 units,
+            // decimal place redrawn from [1,6] every `block` values
+            if (i % s->block == 0) dp_block = 1 + (int)(rng() % 6);
+            const int64_t span = 2 * (int64_t)s->max_step_units + 1;
+            acc += (int64_t)(rng() % (uint64_t)span) - s->max_step_units;
+            if (acc > 999999) acc = 2 * 999999 - acc;
+            if (acc < -999999) acc = -2 * 999999 - acc;
+            emit(i, acc, dp_block);
+            break;
+        }
+        default:
+            return set_error(FALCON_ERR_INVALID, "unknown generator kind");
+        }
+    }
+    return FALCON_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,49 @@
+// kernels.h -- host-side launch interface of the sm_100a codec kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "falcon_common.cuh"
+
+namespace fb200 {
+
+struct archive_header_bytes {
+    uint8_t b[48];
+};
+
+// Scratch for one compress launch (device memory, owned by the context).
+struct encode_ws {
+    uint64_t* status;             // [n_chunks] look-back words: flag(2b) | value(62b)
+    uint32_t* ticket;             // CTA ticket counter (chunk order)
+    unsigned long long* error;    // (chunk << 8 | code), ~0 = none
+    uint64_t* total;              // archive bytes, written by frame_tables_kernel
+};
+
+// Scratch for one decompress launch.
+struct decode_ws {
+    uint32_t* ticket;             // ticket 0 = frame walker, ticket c+1 = chunk c
+    uint32_t* ready;              // [n_batches] batch frame located (1) or not (0)
+    unsigned long long* abort_at; // first batch the walker could not locate (~0 = none)
+    uint64_t* chunk_off;          // [n_chunks] archive offset of each chunk
+    uint32_t* chunk_size;         // [n_chunks]
+    unsigned long long* error;
+};
+
+uint32_t encode_block_threads(uint32_t chunk_n);
+template <typename T> uint32_t encode_smem_bytes(uint32_t chunk_n);
+template <typename T> uint32_t decode_smem_bytes(uint32_t chunk_n);
+
+template <typename T>
+cudaError_t launch_encode(const T* d_in, const geometry& g, uint8_t* d_out, uint64_t out_cap,
+                          const encode_ws& ws, const archive_header_bytes& hdr, cudaStream_t st);
+
+// d_archive points at the archive's first byte (the 47-byte header), `len` bytes long.
+template <typename T>
+cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry& g, T* d_out,
+                          const decode_ws& ws, cudaStream_t st);
+
+// One-time upload of the pow10 / decade tables (numeric.hpp:17-41, numeric.cpp:10-39).
+cudaError_t upload_tables();
+
+}  // namespace fb200

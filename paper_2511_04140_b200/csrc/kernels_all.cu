@@ -1,0 +1,6 @@
+// kernels_all.cu -- single device translation unit (the tables in tables.cu are
+// referenced by the encode/decode kernels without relocatable device code).
+#define FB200_KERNEL_TU 1
+#include "tables.cu"
+#include "encode.cu"
+#include "decode.cu"

@@ -1,0 +1,43 @@
+// tables.cu -- device copies of the numeric tables.
+//   pow10:  exact 10^0..10^max_alpha built by repeated *10 (numeric.hpp:17-41)
+//   decade: correctly rounded 10^k for k in [min_decade, max_decade], stored as IEEE
+//           bit patterns (numeric.cpp:10-39 builds them with snprintf("1e%d") +
+//           std::from_chars; glibc strtod/strtof are also correctly rounded, so the
+//           tables are bit-identical).
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "kernels.h"
+
+namespace fb200 {
+
+cudaError_t upload_tables() {
+    double p64[23];
+    float p32[11];
+    double d = 1.0;
+    for (int i = 0; i < 23; ++i, d *= 10.0) p64[i] = d;
+    float f = 1.0f;
+    for (int i = 0; i < 11; ++i, f *= 10.0f) p32[i] = f;
+    uint64_t dec64[617];
+    uint32_t dec32[77];
+    char buf[16];
+    for (int k = -308; k <= 308; ++k) {
+        std::snprintf(buf, sizeof buf, "1e%d", k);
+        const double v = std::strtod(buf, nullptr);
+        std::memcpy(&dec64[k + 308], &v, 8);
+    }
+    for (int k = -38; k <= 38; ++k) {
+        std::snprintf(buf, sizeof buf, "1e%d", k);
+        const float v = std::strtof(buf, nullptr);
+        std::memcpy(&dec32[k + 38], &v, 4);
+    }
+    cudaError_t e;
+    if ((e = cudaMemcpyToSymbol(g_pow10_f64, p64, sizeof p64))) return e;
+    if ((e = cudaMemcpyToSymbol(g_pow10_f32, p32, sizeof p32))) return e;
+    if ((e = cudaMemcpyToSymbol(g_decade_f64, dec64, sizeof dec64))) return e;
+    return cudaMemcpyToSymbol(g_decade_f32, dec32, sizeof dec32);
+}
+
+}  // namespace fb200
