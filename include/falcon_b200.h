@@ -138,6 +138,11 @@ falcon_status falcon_decompress_device_async(falcon_ctx* ctx, int precision,
                                              const void* d_archive, uint64_t archive_bytes,
                                              const falcon_archive_info* info, void* d_values,
                                              uint64_t cap_values, void* stream);
+/* Profiling hook: when set (non-null), device-resident calls on ctx record enc_start /
+ * enc_stop right before / after the encode kernel and dec_start / dec_stop around the
+ * decode kernel, on the call's stream.  Pass nulls to clear. */
+falcon_status falcon_ctx_set_kernel_events(falcon_ctx* ctx, void* enc_start, void* enc_stop,
+                                           void* dec_start, void* dec_stop);
 /* Wait for `stream` and report the first error raised by async calls on ctx. */
 falcon_status falcon_ctx_sync(falcon_ctx* ctx, void* stream);
 
@@ -169,6 +174,15 @@ falcon_status falcon_compress_chunk(falcon_ctx* ctx, int precision, const void* 
 falcon_status falcon_decompress_chunk(falcon_ctx* ctx, int precision, const uint8_t* in,
                                       uint64_t len, uint32_t chunk_n, uint32_t count,
                                       void* values);
+
+/* ---- self-test (device pointers): the per-value decimal analysis used by the encoder.
+ * d_full[i] = alpha of v[i] by the exact fast loop (-1 = exception), d_literal[i] = the
+ * literal reference loop (std::round + IEEE division), d_cert[i] = certification of v[i]
+ * against candidate_alpha (0 undecided, 1 certified, 2 certified exception) and d_g[i]
+ * the certified lane integer.  Used by tests/test_gpu_dpds.py against the CPU oracle. */
+falcon_status falcon_selftest_dp(falcon_ctx* ctx, int precision, const void* d_values, uint64_t n,
+                                 int candidate_alpha, int8_t* d_full, int8_t* d_literal,
+                                 int8_t* d_cert, int64_t* d_g, void* stream);
 
 /* ---- synthetic inputs (synthetic.hpp:14-32 kinds; kind 5 = the pinned cfg3 kind) ---- */
 #define FALCON_KIND_WALK 0

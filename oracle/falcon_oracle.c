@@ -300,6 +300,19 @@ OR_DEFINE(f64, double, uint64_t, int64_t, 64, 52, 1023, 0x7ffu, 22, 15, 23, 16, 
 OR_DEFINE(f32, float, uint32_t, int32_t, 32, 23, 127, 0xffu, 10, 6, 11, 7, 0x1p-23f,
           -38, 38, g_dec32, p32, bits32, val32, fabsf, roundf, llroundf)
 
+void or_dp_alpha_batch(int prec, const void* values, uint64_t n, int8_t* alpha_out) {
+    for (uint64_t i = 0; i < n; ++i) {
+        uint8_t a, b;
+        if (prec == 0) {
+            or_dp_ds_f64(((const double*)values)[i], &a, &b);
+            alpha_out[i] = (a > 22 || b > 15) ? -1 : (int8_t)a;
+        } else {
+            or_dp_ds_f32(((const float*)values)[i], &a, &b);
+            alpha_out[i] = (a > 10 || b > 6) ? -1 : (int8_t)a;
+        }
+    }
+}
+
 /* max_encoded_chunk_size (chunk_codec.hpp:36-41) */
 size_t or_max_encoded_chunk_size(int prec, size_t n) {
     const size_t lane = prec == 0 ? 8 : 4, width = prec == 0 ? 64 : 32;

@@ -69,6 +69,8 @@ int or_floor_log10_f32(float v);
 /* dp_ds_calculate_counted (numeric.hpp:108-140): returns iterations. */
 int or_dp_ds_f64(double v, uint8_t* alpha, uint8_t* beta);
 int or_dp_ds_f32(float v, uint8_t* alpha, uint8_t* beta);
+/* Batch form: alpha of each value, -1 for the exception path (numeric.hpp:88-94). */
+void or_dp_alpha_batch(int prec, const void* values, uint64_t n, int8_t* alpha_out);
 /* decimal_round_scale (numeric.hpp:150-156); returns OR_E_SCALE_RANGE on overflow. */
 int or_round_scale_f64(double v, int alpha, int64_t* out);
 int or_round_scale_f32(float v, int alpha, int64_t* out);

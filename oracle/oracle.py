@@ -76,6 +76,9 @@ class Oracle:
                                             C.c_uint64, C.POINTER(C.c_uint64),
                                             C.POINTER(C.c_uint64)]
         L.or_synth_fill.argtypes = [C.c_int, C.POINTER(_Spec), C.c_void_p, C.c_uint64]
+        L.or_dp_alpha_batch.argtypes = [C.c_int, C.c_void_p, C.c_uint64, C.c_void_p]
+        L.or_round_scale_f64.argtypes = [C.c_double, C.c_int, C.POINTER(C.c_int64)]
+        L.or_round_scale_f32.argtypes = [C.c_float, C.c_int, C.POINTER(C.c_int64)]
 
     def message(self, code: int) -> str:
         return self.lib.or_error_message(code).decode()
@@ -93,6 +96,19 @@ class Oracle:
         f = self.lib.or_dp_ds_f64 if prec == F64 else self.lib.or_dp_ds_f32
         it = f(v, C.byref(a), C.byref(b))
         return a.value, b.value, it
+
+    def dp_alpha_batch(self, values: np.ndarray) -> np.ndarray:
+        prec = F64 if values.dtype == np.float64 else F32
+        v = np.ascontiguousarray(values)
+        out = np.empty(len(v), np.int8)
+        self.lib.or_dp_alpha_batch(prec, _ptr(v), len(v), _ptr(out))
+        return out
+
+    def round_scale(self, v: float, alpha: int, prec: int = F64):
+        g = C.c_int64()
+        f = self.lib.or_round_scale_f64 if prec == F64 else self.lib.or_round_scale_f32
+        rc = f(v, alpha, C.byref(g))
+        return None if rc else g.value
 
     def floor_log10(self, v: float, prec: int = F64) -> int:
         f = self.lib.or_floor_log10_f64 if prec == F64 else self.lib.or_floor_log10_f32

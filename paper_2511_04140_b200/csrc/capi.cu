@@ -45,15 +45,6 @@ falcon_status error_from_device(unsigned long long word, uint64_t cpb, bool batc
     return set_error(device_error_status(code), msg);
 }
 
-encode_ws ctx_encode_ws(falcon_ctx* ctx, uint64_t* d_total) {
-    encode_ws ws;
-    ws.status = ctx->enc_status.as<uint64_t>();
-    ws.ticket = reinterpret_cast<uint32_t*>(misc_at(ctx, kEncTicket));
-    ws.error = reinterpret_cast<unsigned long long*>(misc_at(ctx, kEncError));
-    ws.total = d_total ? d_total : reinterpret_cast<uint64_t*>(misc_at(ctx, kEncTotal));
-    return ws;
-}
-
 decode_ws ctx_decode_ws(falcon_ctx* ctx) {
     decode_ws ws;
     ws.ticket = reinterpret_cast<uint32_t*>(misc_at(ctx, kDecTicket));
@@ -70,15 +61,22 @@ falcon_status enqueue_compress(falcon_ctx* ctx, int prec, const void* d_values, 
                                uint64_t* d_total, cudaStream_t st, geometry& g) {
     FB_TRY(validate_options(chunk_n, bv));
     FB_TRY(make_geometry(n, chunk_n, bv, 47, g));
-    FB_TRY(ctx->enc_status.ensure(g.n_chunks * sizeof(uint64_t) + 8));
+    const size_t scratch = prec == FALCON_F64 ? encode_scratch_bytes<double>(g) : encode_scratch_bytes<float>(g);
+    FB_TRY(ctx->enc_status.ensure(scratch));
     const archive_header_bytes hdr = header_bytes_of(prec, chunk_n, bv, n, g.n_batches);
     if (cap < 47) return set_error(FALCON_ERR_CAPACITY, "output capacity too small for the header");
-    const encode_ws ws = ctx_encode_ws(ctx, d_total);
+    uint32_t* ticket = reinterpret_cast<uint32_t*>(misc_at(ctx, kEncTicket));
+    auto* err = reinterpret_cast<unsigned long long*>(misc_at(ctx, kEncError));
+    uint64_t* total = d_total ? d_total : reinterpret_cast<uint64_t*>(misc_at(ctx, kEncTotal));
+    const encode_ws ws = prec == FALCON_F64 ? carve_encode_ws<double>(ctx->enc_status.p, g, ticket, err, total)
+                                            : carve_encode_ws<float>(ctx->enc_status.p, g, ticket, err, total);
     cudaError_t e = prec == FALCON_F64
                         ? launch_encode<double>(static_cast<const double*>(d_values), g,
-                                                static_cast<uint8_t*>(d_out), cap, ws, hdr, st)
+                                                static_cast<uint8_t*>(d_out), cap, ws, hdr, st,
+                                                ctx->prof_ev[0], ctx->prof_ev[1])
                         : launch_encode<float>(static_cast<const float*>(d_values), g,
-                                               static_cast<uint8_t*>(d_out), cap, ws, hdr, st);
+                                               static_cast<uint8_t*>(d_out), cap, ws, hdr, st,
+                                               ctx->prof_ev[0], ctx->prof_ev[1]);
     if (e != cudaSuccess) return set_error(FALCON_ERR_CUDA, std::string("encode launch: ") + cudaGetErrorString(e));
     return FALCON_OK;
 }
@@ -136,9 +134,11 @@ falcon_status enqueue_decompress(falcon_ctx* ctx, int prec, const void* d_archiv
     const decode_ws ws = ctx_decode_ws(ctx);
     cudaError_t e = prec == FALCON_F64
                         ? launch_decode<double>(static_cast<const uint8_t*>(d_archive), bytes, g,
-                                                static_cast<double*>(d_values), ws, st)
+                                                static_cast<double*>(d_values), ws, st,
+                                                ctx->prof_ev[2], ctx->prof_ev[3])
                         : launch_decode<float>(static_cast<const uint8_t*>(d_archive), bytes, g,
-                                               static_cast<float*>(d_values), ws, st);
+                                               static_cast<float*>(d_values), ws, st,
+                                               ctx->prof_ev[2], ctx->prof_ev[3]);
     if (e != cudaSuccess) return set_error(FALCON_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
     return FALCON_OK;
 }
@@ -290,6 +290,17 @@ falcon_status falcon_decompress_device(falcon_ctx* ctx, int precision, const voi
     return FALCON_OK;
 }
 
+falcon_status falcon_ctx_set_kernel_events(falcon_ctx* ctx, void* enc_start, void* enc_stop,
+                                           void* dec_start, void* dec_stop) {
+    if (!ctx) return set_error(FALCON_ERR_INVALID, "null context");
+    std::lock_guard<std::mutex> lock(ctx->api_mutex);
+    ctx->prof_ev[0] = static_cast<cudaEvent_t>(enc_start);
+    ctx->prof_ev[1] = static_cast<cudaEvent_t>(enc_stop);
+    ctx->prof_ev[2] = static_cast<cudaEvent_t>(dec_start);
+    ctx->prof_ev[3] = static_cast<cudaEvent_t>(dec_stop);
+    return FALCON_OK;
+}
+
 falcon_status falcon_ctx_sync(falcon_ctx* ctx, void* stream) {
     if (!ctx) return set_error(FALCON_ERR_INVALID, "null context");
     std::lock_guard<std::mutex> lock(ctx->api_mutex);
@@ -307,6 +318,17 @@ falcon_status falcon_ctx_sync(falcon_ctx* ctx, void* stream) {
     // batch index of an async error is not recoverable without the geometry; report the text
     FB_TRY(error_from_device(errs[0], 1, false));
     FB_TRY(error_from_device(errs[1], 1, false));
+    return FALCON_OK;
+}
+
+falcon_status falcon_selftest_dp(falcon_ctx* ctx, int precision, const void* d_values, uint64_t n,
+                                 int candidate_alpha, int8_t* d_full, int8_t* d_literal,
+                                 int8_t* d_cert, int64_t* d_g, void* stream) {
+    if (!ctx) return set_error(FALCON_ERR_INVALID, "null context");
+    device_guard dg(ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    FB_CUDA(launch_selftest_dp(precision, d_values, n, candidate_alpha, d_full, d_literal, d_cert, d_g, st));
+    FB_CUDA(cudaStreamSynchronize(st));
     return FALCON_OK;
 }
 

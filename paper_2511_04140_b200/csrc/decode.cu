@@ -356,7 +356,7 @@ uint32_t decode_smem_bytes(uint32_t chunk_n) {
 
 template <typename T>
 cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry& g, T* d_out,
-                          const decode_ws& ws, cudaStream_t st) {
+                          const decode_ws& ws, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
     cudaError_t e;
     if (g.n_chunks == 0) return cudaSuccess;
     if ((e = cudaMemsetAsync(ws.ticket, 0, sizeof(uint32_t), st))) return e;
@@ -366,14 +366,16 @@ cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry
     const uint32_t smem = decode_smem_bytes<T>(g.chunk_n);
     auto kern = threads <= 256 ? decode_chunks_kernel<T, 256> : decode_chunks_kernel<T, 1024>;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    if (ev0 && (e = cudaEventRecord(ev0, st))) return e;
     kern<<<(unsigned)(g.n_chunks + 1), threads, smem, st>>>(d_archive, len, g, d_out, ws);
-    return cudaGetLastError();
+    if ((e = cudaGetLastError())) return e;
+    return ev1 ? cudaEventRecord(ev1, st) : cudaSuccess;
 }
 
 template cudaError_t launch_decode<double>(const uint8_t*, uint64_t, const geometry&, double*,
-                                           const decode_ws&, cudaStream_t);
+                                           const decode_ws&, cudaStream_t, cudaEvent_t, cudaEvent_t);
 template cudaError_t launch_decode<float>(const uint8_t*, uint64_t, const geometry&, float*,
-                                          const decode_ws&, cudaStream_t);
+                                          const decode_ws&, cudaStream_t, cudaEvent_t, cudaEvent_t);
 template uint32_t decode_smem_bytes<double>(uint32_t);
 template uint32_t decode_smem_bytes<float>(uint32_t);
 

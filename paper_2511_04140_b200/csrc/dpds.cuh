@@ -1,0 +1,165 @@
+// dpds.cuh -- exact, instruction-lean restatement of the per-value decimal analysis
+// (dp_ds_calculate_counted, reference numeric.hpp:108-140).  Included only by the
+// kernel translation unit.  Every function returns exactly what the reference loop
+// decides; DESIGN.md "Exact fast analysis" carries the proofs, and
+// tests/test_gpu_dpds.py checks them against the CPU oracle on 10^8 inputs.
+//
+// (1) Gap test.  The reference accepts scale a when |s - round(s)| <= |s| * 2^-52 with
+//     s = RN(v * 10^a).  Writing s = M * 2^(E-52) (M in [2^52, 2^53)) and G for the
+//     distance of s to the nearest integer in ulps, the test is G * 2^(E-52) <=
+//     M * 2^(E-104), i.e. G <= M / 2^52 in [1, 2): it holds iff G <= 1.  For |s| < 1
+//     it holds only for s = +-(1 - 2^-53) (nearest +-1).  So the test is a mask on the
+//     fraction bits of s, and the rounded integer N is read off the same bits.
+// (2) Reconstruction check.  The reference rejects v unless RN(N / 10^a) == v.  Within
+//     the loop bounds (beta <= max_beta, so |s| < 10^15 for f64), e = N - v * 10^a is a
+//     multiple of 2^(ev-52+a) of magnitude < 2^53 of those units, so fma(-v, p, N)
+//     yields e exactly, and RN(N/p) == v  <=>  |e| < p * ulp(v)/2 (halved below a power
+//     of two), ties resolved to even -- all exact comparisons.  f32 uses a double
+//     residual (the 24x24-bit product is exact in double).
+// (3) Certification at a candidate scale A (alpha0 <= A <= loop bound).  If the
+//     reference test passes at some alpha_v <= A, then v*10^A lies within 3.5 ulp of
+//     N_v * 10^(A - alpha_v) and that integer is the N found at A (|s| < 2^50 makes the
+//     ulp <= 1/8).  Hence when the test passes at A: alpha_v <= A, and the
+//     reconstruction check at A divides the same real number N_v / 10^alpha_v, so it
+//     gives the same verdict.  When the test fails at A nothing is concluded.
+#pragma once
+
+#include "falcon_common.cuh"
+
+namespace fb200 {
+
+template <typename T> struct fpx;
+
+template <> struct fpx<double> {
+    using B = uint64_t;
+    using S = int64_t;
+    static constexpr int MB = 52;                 // mantissa bits
+    static constexpr B MANT = (B(1) << 52) - 1;
+    static constexpr B SIGN = B(1) << 63;
+    static constexpr B EXPF = B(0x7ff) << 52;
+    static constexpr int BIAS = 1023;
+    static constexpr unsigned EMASK = 0x7ffu;
+    static constexpr int MAXA = 22, MAXB = 15, MIND = -308;
+    __device__ static double pow10(int a) { return g_pow10_f64[a]; }
+    __device__ static B dec(int k) { return g_decade_f64[k - MIND]; }
+    __device__ static B bits(double v) { return (B)__double_as_longlong(v); }
+    __device__ static double val(B b) { return __longlong_as_double((long long)b); }
+    __device__ static double rint_(double x) { return rint(x); }
+    __device__ static S to_int(double N) { return (S)__double2ll_rz(N); }
+    // exact reconstruction verdict RN(N / p) == v from the exact residual (2)
+    __device__ static bool recon_ok(double v, double p, double N) {
+        const B eb = bits(__fma_rn(-v, p, N));   // exact: N - v*p
+        const B ae = eb & ~SIGN;
+        const B vb = bits(v);
+        const B halve = (((eb ^ vb) & SIGN) != 0 && (vb & MANT) == 0) ? 1 : 0;
+        // H = p * 2^(ev - 53) (halved below a power of two) by exponent arithmetic
+        const B hb = bits(p) + (((vb >> MB) & EMASK) - (B)(BIAS + MB + 1) - halve << MB);
+        return ae == 0 || ae < hb || (ae == hb && (vb & 1) == 0);
+    }
+};
+
+template <> struct fpx<float> {
+    using B = uint32_t;
+    using S = int32_t;
+    static constexpr int MB = 23;
+    static constexpr B MANT = (B(1) << 23) - 1;
+    static constexpr B SIGN = B(1) << 31;
+    static constexpr B EXPF = B(0xff) << 23;
+    static constexpr int BIAS = 127;
+    static constexpr unsigned EMASK = 0xffu;
+    static constexpr int MAXA = 10, MAXB = 6, MIND = -38;
+    __device__ static float pow10(int a) { return g_pow10_f32[a]; }
+    __device__ static B dec(int k) { return g_decade_f32[k - MIND]; }
+    __device__ static B bits(float v) { return __float_as_uint(v); }
+    __device__ static float val(B b) { return __uint_as_float(b); }
+    __device__ static float rint_(float x) { return rintf(x); }
+    __device__ static S to_int(float N) { return (S)__float2int_rz(N); }
+    __device__ static bool recon_ok(float v, float p, float N) {
+        // residual in double: v*p (24 x 24 bits) is exact and N - v*p fits in 53 bits
+        const uint64_t eb = (uint64_t)__double_as_longlong(__fma_rn(-(double)v, (double)p, (double)N));
+        const uint64_t ae = eb & ~(1ull << 63);
+        const B vb = bits(v);
+        const uint64_t halve = (((eb >> 63) != (vb >> 31)) && (vb & MANT) == 0) ? 1 : 0;
+        // H = p * 2^(ev - 24) as a double
+        const uint64_t hb = (uint64_t)__double_as_longlong((double)p) +
+                            ((uint64_t)((vb >> MB) & EMASK) - (uint64_t)(BIAS + MB + 1) - halve << 52);
+        return ae == 0 || ae < hb || (ae == hb && (vb & 1) == 0);
+    }
+};
+
+// exact floor_log10 of a positive normal magnitude (numeric.hpp:54-66): with
+// k0 = (floor_log2 * 78913) >> 18 the decade-table answer is always k0 or k0 + 1
+// (checked exhaustively over every binade of both formats).
+template <typename T>
+__device__ __forceinline__ int mag_of(typename fpx<T>::B m) {
+    using X = fpx<T>;
+    const int e2 = (int)(m >> X::MB) - X::BIAS;
+    const int k0 = (e2 * 78913) >> 18;
+    return k0 + (m >= X::dec(k0 + 1) ? 1 : 0);
+}
+
+// (1): the reference gap test for s (|s - round(s)| <= |s| * 2^-52, numeric.hpp:127-129)
+// holds iff s is within one ulp of an integer; rint() finds that integer (ties cannot
+// pass), the difference is exact, and the comparison is on bit patterns.  On success
+// *N = round_half_away(s).
+template <typename T>
+__device__ __forceinline__ bool near_integer(T s, T* N) {
+    using X = fpx<T>;
+    using B = typename X::B;
+    const T r = X::rint_(s);
+    const B sb = X::bits(s);
+    const B ef = sb & X::EXPF;
+    const B ulp = ef - ((B)X::MB << X::MB);        // bits of 2^(E - MB)
+    const B ad = X::bits(s - r) & ~X::SIGN;         // exact |s - rint(s)|
+    *N = r;
+    return ef > ((B)X::MB << X::MB) && ad <= ulp;
+}
+
+// Reference loop (numeric.hpp:108-140) with (1) and (2).  alpha_v or -1 (exception).
+template <typename T>
+__device__ __noinline__ int dp_alpha_full(T v) {
+    using X = fpx<T>;
+    using B = typename X::B;
+    const B b = X::bits(v);
+    const B m = b & ~X::SIGN;
+    if (m == 0) return (b & X::SIGN) ? -1 : 0;
+    const B ef = b & X::EXPF;
+    if (ef == 0 || ef == X::EXPF) return -1;
+    const int mag = mag_of<T>(m);
+    int alpha = mag < 0 ? -mag : 0;
+    const int lim0 = X::MAXB - 1 - mag;
+    const int limit = lim0 < X::MAXA ? lim0 : X::MAXA;
+    for (; alpha <= limit; ++alpha) {
+        const T p = X::pow10(alpha);
+        T N;
+        if (near_integer<T>(mul_rn(v, p), &N)) return X::recon_ok(v, p, N) ? alpha : -1;
+    }
+    return -1;
+}
+
+enum : int { CERT_UNDECIDED = 0, CERT_OK = 1, CERT_EXC = 2 };
+
+// (3): decide v against candidate scale A (0 <= A <= max_alpha).  CERT_OK: alpha_v <= A
+// and v is not an exception, *g = round_half_away(v*10^A).  CERT_EXC: v is an
+// exception.  CERT_UNDECIDED: run dp_alpha_full.
+template <typename T>
+__device__ __forceinline__ int dp_certify(T v, int A, T p, typename fpx<T>::S* g) {
+    using X = fpx<T>;
+    using B = typename X::B;
+    const B b = X::bits(v);
+    const B m = b & ~X::SIGN;
+    const B ef = b & X::EXPF;
+    *g = 0;
+    if (m == 0) return (b & X::SIGN) ? CERT_EXC : CERT_OK;  // -0 -> exception; +0 -> alpha 0
+    if (ef == 0 || ef == X::EXPF) return CERT_EXC;           // subnormal, inf, nan
+    const int mag = mag_of<T>(m);
+    // A must lie inside the reference loop's range: alpha0 = max(0, -mag) <= A and
+    // beta = A + mag + 1 <= max_beta
+    if (A < -mag || A + mag > X::MAXB - 1) return CERT_UNDECIDED;
+    T N;
+    if (!near_integer<T>(mul_rn(v, p), &N)) return CERT_UNDECIDED;
+    *g = X::to_int(N);
+    return X::recon_ok(v, p, N) ? CERT_OK : CERT_EXC;
+}
+
+}  // namespace fb200

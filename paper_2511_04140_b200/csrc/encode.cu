@@ -1,24 +1,27 @@
 // encode.cu -- fused single-pass Falcon compress for sm_100a.
 //
-// One CTA encodes one chunk (chunk_n values: z1 + (chunk_n-1) delta lanes) and
-// writes it straight into its final archive position:
+// One CTA encodes one chunk (chunk_n values: z1 + (chunk_n-1) delta lanes) straight
+// into its final archive position.  Thread t owns the "byte column" t: delta lanes
+// 8t..8t+7 (values 8t+1..8t+8), which is exactly byte t of every bit-plane row
+// (FORMAT.md:79-84), so planes come out of per-thread 8x8 bit transposes.
 //
-//   load    chunk values -> padded smem                       (coalesced 8/4-B loads)
-//   analyze dp_ds per value -> alpha_max, any-exception, max|v| (warp redux + smem)
-//           (numeric.hpp:108-140, transform.hpp:47-68)
-//   delta   g_i = llround(v*10^a) | zigzag(bits); z_i = zigzag(g_i - g_{i-1})
-//           (transform.hpp:72-89), thread t owns lanes 8t..8t+7 ("byte column" t)
-//   planes  per 8 bit-planes: pack one byte of each of the 8 lanes, 8x8 bit transpose
-//           -> the thread's byte of each plane row (bitplane.hpp:64-90 semantics)
-//   size    per-row zero-byte count via ballot, dense/sparse choice, row offsets
-//           (bitplane.hpp:113-122, chunk_codec.hpp:59-73)
-//   place   decoupled look-back over chunk sizes in ticket order -> archive offset;
-//           the batch frame's table bytes are added analytically (container.cpp:88-111)
-//   emit    chunk image built in smem at the destination's 16-B phase, then stored
-//           with 16-B vector stores (sparse rows compacted with ballot prefix counts)
+//   load     each thread loads its 8 values + the preceding one into registers
+//   analyze  phase 1: exact dp_ds loop on one sample value per thread -> A0 = max
+//            phase 2: every value certified against A0 (dpds.cuh (3)); the few that
+//            cannot be certified run the exact loop.  alpha_max, exceptions, max|v|
+//            (numeric.hpp:108-140, transform.hpp:47-68) -- bit-identical results
+//   delta    g = round(v*10^alpha_max) (reused from certification) or
+//            zigzag(bits(v)); z = zigzag(g_i - g_{i-1}) (transform.hpp:72-89)
+//   planes   per 8 bit positions: 8x8 bit transpose -> this thread's row bytes
+//   size     warp 0: per-row zero-byte counts, dense/sparse choice, row offsets
+//            (bitplane.hpp:113-122, chunk_codec.hpp:59-73), decoupled look-back over
+//            chunk sizes in ticket order; batch-frame tables are added analytically
+//   emit     one warp per row into smem staging at the destination's 16-B phase:
+//            dense rows copied, sparse rows compacted with ballot ranks
+//   store    16-B vector stores; bytes only at the two ragged ends
 //
-// A second, tiny kernel (frame_tables) writes the per-batch [u32 count][u32 size..]
-// tables and the 47-byte header once every chunk's prefix is known.
+// frame_tables_kernel then writes the [u32 count][u32 size...] tables and the header.
+#include "dpds.cuh"
 #include "falcon_common.cuh"
 #include "kernels.h"
 
@@ -29,7 +32,6 @@ namespace {
 constexpr uint64_t kFlagAgg = 1ull << 62;
 constexpr uint64_t kFlagInc = 2ull << 62;
 constexpr uint64_t kValMask = (1ull << 62) - 1;
-
 
 template <typename B>
 __device__ __forceinline__ B warp_or(B v);
@@ -60,86 +62,124 @@ __device__ __forceinline__ uint32_t warp_max(uint32_t v) {
 __device__ __forceinline__ int bit_width(uint64_t x) { return x ? 64 - __clzll((long long)x) : 0; }
 __device__ __forceinline__ int bit_width(uint32_t x) { return x ? 32 - __clz((int)x) : 0; }
 
-// byte s of lane value x (s < sizeof(B))
-__device__ __forceinline__ uint32_t byte_of(uint64_t x, int s) {
-    return (uint32_t)(x >> (8 * s)) & 0xffu;
-}
+__device__ __forceinline__ uint32_t byte_of(uint64_t x, int s) { return (uint32_t)(x >> (8 * s)) & 0xffu; }
 __device__ __forceinline__ uint32_t byte_of(uint32_t x, int s) { return (x >> (8 * s)) & 0xffu; }
 
 }  // namespace
 
-// bytes of the values region, which is reused as the chunk-image staging buffer
+// bytes of the chunk-image staging region
 template <typename T>
-__host__ __device__ __forceinline__ uint32_t encode_region_bytes(uint32_t chunk_n) {
+__host__ __device__ __forceinline__ uint32_t encode_stage_bytes(uint32_t chunk_n) {
     using tr = lane_traits<T>;
     const uint32_t nc = (chunk_n - 1) / 8;
-    const uint32_t vals = (uint32_t)((pidx(chunk_n) + 1) * sizeof(T) + 15) & ~15u;
-    const uint32_t stage = (uint32_t)(tr::header + (tr::width + 7) / 8 + tr::width * nc + 16 + 15) & ~15u;
-    return vals > stage ? vals : stage;
+    return (uint32_t)(tr::header + (tr::width + 7) / 8 + tr::width * nc + 32 + 15) & ~15u;
 }
 
 template <typename T, int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1) encode_chunks_kernel(const T* __restrict__ in, geometry g,
-                                                             uint8_t* __restrict__ out,
-                                                             uint64_t out_cap, encode_ws ws) {
+__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1)
+    encode_chunks_kernel(const T* __restrict__ in, geometry g, uint8_t* __restrict__ out,
+                         uint64_t out_cap, encode_ws ws) {
     using tr = lane_traits<T>;
+    using X = fpx<T>;
     using B = typename tr::B;
     using S = typename tr::S;
-    constexpr int W = tr::width;
     constexpr int HDR = tr::header;
 
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t n = g.chunk_n;
     const int NC = (int)((n - 1) / 8);  // row bytes = byte columns
+    const int BM = NC / 8;              // sparse bitmap bytes
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = blockDim.x >> 5;
 
-    // smem carve-up (sizes must match encode_smem_bytes())
-    const uint32_t vals_region = encode_region_bytes<T>(n);
-    T* s_v = reinterpret_cast<T*>(smem);
-    uint8_t* s_stage = smem;                                    // aliases s_v after transform
-    uint8_t* s_rows = smem + vals_region;                       // [W][NC]
-    uint16_t* s_nzw = reinterpret_cast<uint16_t*>(s_rows + ((W * NC + 15) & ~15));  // [W][nwarps]
+    uint8_t* s_stage = smem;                                  // chunk image
+    // [block][thread] u64: byte k of entry (s, t) = row byte t of bit plane 8s+k
+    uint64_t* s_planes = reinterpret_cast<uint64_t*>(smem + encode_stage_bytes<T>(n));
+    const int PT = (int)blockDim.x;
 
-    __shared__ uint32_t s_ticket;
-    __shared__ uint32_t s_amax[32], s_exc[32], s_warpw[32];
+    __shared__ int s_a0[32], s_amax[32];
+    __shared__ uint32_t s_exc[32], s_warpw[32];
     __shared__ B s_vmax[32];
-    __shared__ uint32_t s_nz[64];
     __shared__ uint32_t s_rowoff[64];
-    __shared__ uint64_t s_dense, s_off;
+    __shared__ uint32_t s_nzc[32][16];   // per warp: 8-bit nonzero-byte counters, 4 planes/word
+    __shared__ uint16_t s_wpre[64 * 32]; // nonzero bytes of plane p in warps before w
+    __shared__ uint64_t s_dense;
     __shared__ uint32_t s_size;
     __shared__ B s_z1;
 
-    if (tid == 0) s_ticket = atomicAdd(ws.ticket, 1u);
-    for (int i = tid; i < 64; i += blockDim.x) s_nz[i] = 0;
-    __syncthreads();
-    const uint64_t c = s_ticket;
+    const uint64_t c = blockIdx.x;
     const uint64_t b = g.batch_of(c);
     const uint32_t ci = (uint32_t)(c - b * g.cpb);
     const uint64_t bcount = g.values_in(b);
     const uint64_t v0 = b * g.batch_values + (uint64_t)ci * n;
     const uint64_t left = bcount - (uint64_t)ci * n;
-    const uint32_t len = left < n ? (uint32_t)left : n;   // short final chunk: +0.0 padding
+    const uint32_t len = left < n ? (uint32_t)left : n;  // short final chunk: +0.0 padding
+    const bool active = tid < NC;
 
-    // ---- load (pipeline.hpp:205-215 padding) ----
-    for (uint32_t i = tid; i < n; i += blockDim.x) s_v[pidx(i)] = i < len ? in[v0 + i] : T(0);
-    __syncthreads();
+    // ---- load: values 8t .. 8t+8 (pipeline.hpp:205-215 zero padding) ----
+    T v[8];
+    T vprev = T(0);
+    {
+        const T* src = in + v0;
+        const uint32_t i0 = 8u * (uint32_t)tid;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = (active && i0 + 1 + j < len) ? __ldg(src + i0 + 1 + j) : T(0);
+        if (active && i0 < len) vprev = __ldg(src + i0);
+    }
 
-    // ---- analyze (transform.hpp:47-68) ----
-    int amax = 0;
-    bool exc = false;
-    B vmax = 0;
-    for (uint32_t i = tid; i < n; i += blockDim.x) {
-        const T v = s_v[pidx(i)];
-        const int a = dp_alpha<T>(v);
-        exc |= a < 0;
-        amax = a > amax ? a : amax;
-        const B m = bits_of(v) & ~((B)1 << (W - 1));
-        vmax = m > vmax ? m : vmax;
+    // ---- analyze, phase 1: exact loop on one sample per thread -> A0 ----
+    int a1 = active ? dp_alpha_full<T>(v[0]) : 0;
+    if (tid == 0) {  // value 0 is analysed by thread 0 only
+        const int az = dp_alpha_full<T>(vprev);
+        a1 = (a1 < 0 || az < 0) ? -1 : (az > a1 ? az : a1);
     }
     {
-        const uint32_t wa = __reduce_max_sync(0xffffffffu, (uint32_t)amax);
+        const bool we = __any_sync(0xffffffffu, a1 < 0);
+        const int wa = (int)__reduce_max_sync(0xffffffffu, (uint32_t)(a1 < 0 ? 0 : a1));
+        if (lane == 0) {
+            s_a0[warp] = wa;
+            s_exc[warp] = we;
+        }
+    }
+    __syncthreads();
+    int A0 = 0;
+    bool exc = false;
+    for (int i = 0; i < nwarps; ++i) {
+        A0 = s_a0[i] > A0 ? s_a0[i] : A0;
+        exc |= s_exc[i] != 0;
+    }
+
+    // ---- analyze, phase 2: certify every value against A0 ----
+    const T pA0 = X::pow10(A0);
+    S gc[8];
+    uint32_t redo = 0;  // lanes whose lane integer must be recomputed at alpha_max
+    int afb = A0;       // max over values decided by the exact loop
+    B vmax = 0;
+    if (active) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const B mb = X::bits(v[j]) & ~X::SIGN;
+            vmax = mb > vmax ? mb : vmax;
+            gc[j] = 0;
+            if (exc) continue;  // the chunk already takes the raw path
+            const int r = dp_certify<T>(v[j], A0, pA0, &gc[j]);
+            if (r == CERT_EXC) {
+                exc = true;
+            } else if (r == CERT_UNDECIDED) {
+                redo |= 1u << j;
+                const int av = dp_alpha_full<T>(v[j]);
+                if (av < 0) exc = true;
+                else afb = av > afb ? av : afb;
+            }
+        }
+        if (tid == 0) {
+            const B mb = X::bits(vprev) & ~X::SIGN;
+            vmax = mb > vmax ? mb : vmax;
+        }
+    }
+    {
         const bool we = __any_sync(0xffffffffu, exc);
+        const int wa = (int)__reduce_max_sync(0xffffffffu, (uint32_t)afb);
         const B wv = warp_max<B>(vmax);
         if (lane == 0) {
             s_amax[warp] = wa;
@@ -148,72 +188,64 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1) encode_ch
         }
     }
     __syncthreads();
-    amax = 0;
-    exc = false;
+    int amax = A0;
     vmax = 0;
-    for (int w = 0; w < nwarps; ++w) {
-        amax = (int)s_amax[w] > amax ? (int)s_amax[w] : amax;
-        exc |= s_exc[w] != 0;
-        vmax = s_vmax[w] > vmax ? s_vmax[w] : vmax;
+    for (int i = 0; i < nwarps; ++i) {
+        amax = s_amax[i] > amax ? s_amax[i] : amax;
+        exc |= s_exc[i] != 0;
+        vmax = s_vmax[i] > vmax ? s_vmax[i] : vmax;
     }
     bool case2 = exc;
     int bhat = 0;
-    if (!case2) {
+    if (!case2) {  // transform.hpp:62-65
         bhat = vmax == 0 ? 0 : amax + floor_log10_bits(vmax) + 1;
         case2 = amax > tr::max_alpha || bhat > tr::max_beta;
     }
     const uint32_t hA = case2 ? tr::exc_alpha : (uint32_t)amax;
     const uint32_t hB = case2 ? tr::exc_beta : (uint32_t)bhat;
 
-    // ---- forward transform in byte-column layout (transform.hpp:72-89) ----
-    const T scale = pow10_of(T{}, case2 ? 0 : amax);
+    // ---- forward transform (transform.hpp:72-89) ----
+    const T scale = X::pow10(case2 ? 0 : amax);
     bool range_err = false;
-    auto lane_g = [&](T v) -> B {
-        if (case2) return zigzag<B>(bits_of(v));
-        const T s = mul_rn(v, scale);
-        range_err |= !(fabs(s) < (T)0x1p62);                  // numeric.hpp:153-154
+    auto lane_g = [&](T x) -> B {
+        if (case2) return zigzag<B>(X::bits(x));
+        const T s = mul_rn(x, scale);
+        range_err |= !(fabs(s) < (T)0x1p62);  // numeric.hpp:153-154
         return (B)(S)llround_away(s);
     };
     B z[8];
     B orv = 0;
-    if (tid < NC) {
-        B gp = lane_g(s_v[pidx(8 * tid)]);
+    {
+        const bool reuse = !case2 && amax == A0;
+        B gp = lane_g(vprev);
         if (tid == 0) s_z1 = gp;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const B gj = lane_g(s_v[pidx(8 * tid + 1 + j)]);
-            z[j] = zigzag<B>((B)(gj - gp));
+            const B gj = (reuse && !((redo >> j) & 1)) ? (B)gc[j] : lane_g(v[j]);
+            z[j] = active ? zigzag<B>((B)(gj - gp)) : (B)0;
             gp = gj;
             orv |= z[j];
         }
-    } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) z[j] = 0;
     }
     if (range_err) record_error(ws.error, c, DEV_E_SCALE);
 
-    // ---- bit planes: warp-local width, 8x8 transposes, zero-byte counts ----
+    // ---- bit planes: warp-local width, 8x8 transposes -> s_planes, nonzero counts ----
     const int warp_w = bit_width(warp_or<B>(orv));
     const int nblk = (warp_w + 7) >> 3;
-    for (int s = 0; s < nblk; ++s) {
-        // lane j's byte s at byte (7-j): the transpose then yields, in byte k, the
-        // row byte of bit plane 8s+k with lane j at bit 7-j (MSB-first, FORMAT.md:81-84)
+    for (int sb = 0; sb < nblk; ++sb) {
+        // lane j's byte sb at byte (7-j): byte k of the transpose is the row byte of bit
+        // plane 8sb+k with lane j at bit 7-j (MSB-first, FORMAT.md:81-84)
         uint64_t x = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) x |= (uint64_t)byte_of(z[j], s) << (8 * (7 - j));
+        for (int j = 0; j < 8; ++j) x |= (uint64_t)byte_of(z[j], sb) << (8 * (7 - j));
         const uint64_t y = transpose8x8(x);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int p = 8 * s + k;
-            if (p < warp_w) {
-                const uint32_t byte = (uint32_t)(y >> (8 * k)) & 0xffu;
-                if (tid < NC) s_rows[p * NC + tid] = (uint8_t)byte;
-                const uint32_t nzm = __ballot_sync(0xffffffffu, byte != 0);
-                if (lane == 0) {
-                    s_nzw[p * nwarps + warp] = (uint16_t)__popc(nzm);
-                    atomicAdd(&s_nz[p], (uint32_t)__popc(nzm));
-                }
-            }
+        s_planes[sb * PT + tid] = y;
+        // nonzero bytes per plane, 8-bit counters (<= 32 per warp, no carries)
+        const uint32_t lo = __reduce_add_sync(0xffffffffu, __vcmpne4((uint32_t)y, 0u) & 0x01010101u);
+        const uint32_t hi = __reduce_add_sync(0xffffffffu, __vcmpne4((uint32_t)(y >> 32), 0u) & 0x01010101u);
+        if (lane == 0) {
+            s_nzc[warp][2 * sb] = lo;
+            s_nzc[warp][2 * sb + 1] = hi;
         }
     }
     if (lane == 0) s_warpw[warp] = (uint32_t)warp_w;
@@ -223,19 +255,27 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1) encode_ch
     for (int i = 0; i < nwarps; ++i) w = (int)s_warpw[i] > w ? (int)s_warpw[i] : w;
     const int fb = (w + 7) >> 3;
 
-    // ---- sizes, row offsets, look-back (warp 0) ----
+    // ---- sizes and row offsets (warp 0): plane p is row w-1-p ----
     if (warp == 0) {
-        auto row_cost = [&](int p, bool& dense) -> uint32_t {
-            dense = false;
+        uint32_t nz0 = 0, nz1 = 0;  // nonzero bytes of planes `lane` and `lane + 32`
+        for (int q = 0; q < nwarps; ++q) {
+            const int wq = (int)s_warpw[q];
+            const uint32_t c0 = lane < wq ? (s_nzc[q][lane >> 2] >> (8 * (lane & 3))) & 0xffu : 0u;
+            const uint32_t c1 = lane + 32 < wq ? (s_nzc[q][(lane + 32) >> 2] >> (8 * (lane & 3))) & 0xffu : 0u;
+            s_wpre[lane * 32 + q] = (uint16_t)nz0;
+            s_wpre[(lane + 32) * 32 + q] = (uint16_t)nz1;
+            nz0 += c0;
+            nz1 += c1;
+        }
+        auto row_cost = [&](int p, uint32_t nz, bool& dns) -> uint32_t {
+            dns = false;
             if (p >= w) return 0;
-            const uint32_t nz = s_nz[p];
-            const uint32_t zeros = (uint32_t)NC - nz;
-            dense = zeros <= (uint32_t)(NC / 8);                   // bitplane.hpp:113-115
-            return dense ? (uint32_t)NC : (uint32_t)(NC / 8) + nz;  // bitplane.hpp:117-122
+            dns = (uint32_t)NC - nz <= (uint32_t)BM;        // bitplane.hpp:113-115
+            return dns ? (uint32_t)NC : (uint32_t)BM + nz;  // bitplane.hpp:117-122
         };
         bool d0, d1;
-        const uint32_t c0 = row_cost(lane, d0);
-        const uint32_t c1 = row_cost(lane + 32, d1);
+        const uint32_t c0 = row_cost(lane, nz0, d0);
+        const uint32_t c1 = row_cost(lane + 32, nz1, d1);
         // rows are emitted from the highest plane down: offset(p) = sum of cost(p' > p)
         uint32_t s1 = c1, s0 = c0;
 #pragma unroll
@@ -255,51 +295,20 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1) encode_ch
         const uint32_t dm0 = __ballot_sync(0xffffffffu, d0);
         const uint32_t dm1 = __ballot_sync(0xffffffffu, d1);
         const uint32_t size = w ? base + tot1 + tot0 : (uint32_t)HDR;
-
-        // decoupled look-back over chunk sizes, in ticket (= chunk) order
-        uint64_t excl = 0;
-        if (lane == 0) st_relaxed(&ws.status[c], (c == 0 ? kFlagInc : kFlagAgg) | size);
-        if (c > 0) {
-            int64_t j = (int64_t)c - 1;
-            for (;;) {
-                const int64_t idx = j - lane;
-                uint64_t st = idx >= 0 ? ld_relaxed(&ws.status[idx]) : kFlagInc;
-                while (__ballot_sync(0xffffffffu, (st >> 62) == 0) != 0) {
-                    __nanosleep(64);
-                    if ((st >> 62) == 0) st = ld_relaxed(&ws.status[idx]);
-                }
-                const uint32_t inc = __ballot_sync(0xffffffffu, (st >> 62) == 2);
-                uint64_t val = st & kValMask;
-                if (inc) {
-                    const int first = __ffs(inc) - 1;
-                    excl += warp_sum_u64(lane <= first ? val : 0);
-                    break;
-                }
-                excl += warp_sum_u64(val);
-                j -= 32;
-            }
-            if (lane == 0) st_relaxed(&ws.status[c], kFlagInc | (excl + size));
-        }
         if (lane == 0) {
             s_dense = ((uint64_t)dm1 << 32) | dm0;
             s_size = size;
-            s_off = g.chunk_base(c) + excl;
+            ws.sizes[c] = size;
         }
     }
     __syncthreads();
-
     const uint32_t size = s_size;
-    const uint64_t off = s_off;
-    if (off + size > out_cap) {
-        if (tid == 0) record_error(ws.error, c, DEV_E_CAPACITY);
-        return;
-    }
-    const uint32_t a = (uint32_t)(off & 15);
     const uint64_t dense = s_dense;
 
-    // ---- emit the chunk image into staging at the destination's 16-B phase ----
+    // ---- emit the chunk image into staging: every thread writes its column of every
+    //      row; sparse rows place their nonzero bytes by warp prefix + ballot rank ----
     if (tid == 0) {
-        uint8_t* h = s_stage + a;
+        uint8_t* h = s_stage;
         h[0] = (uint8_t)hA;
         h[1] = (uint8_t)hB;
         const B z1 = s_z1;
@@ -309,71 +318,184 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1) encode_ch
         for (int i = 0; i < fb; ++i) h[HDR + i] = (uint8_t)(dense >> (8 * (fb - 1 - i)));
     }
     const uint32_t lt_mask = (1u << lane) - 1u;
-    for (int p = 0; p < w; ++p) {
-        const bool mine = tid < NC && p < (int)s_warpw[warp];
-        const uint32_t byte = mine ? s_rows[p * NC + tid] : 0u;
-        uint8_t* row = s_stage + a + s_rowoff[p];
-        if ((dense >> p) & 1) {
-            if (tid < NC) row[tid] = (uint8_t)byte;
-        } else {
-            const uint32_t nzm = __ballot_sync(0xffffffffu, byte != 0);
-            if (tid < NC && (lane & 7) == 0) row[tid >> 3] = (uint8_t)(__brev(nzm >> lane) >> 24);
-            if (byte != 0) {
-                uint32_t before = 0;
-                for (int q = 0; q < warp; ++q)
-                    before += p < (int)s_warpw[q] ? s_nzw[p * nwarps + q] : 0u;
-                row[NC / 8 + before + __popc(nzm & lt_mask)] = (uint8_t)byte;
+    const int wblk = (w + 7) >> 3;
+    for (int sb = 0; sb < wblk; ++sb) {
+        const uint64_t y = sb < nblk ? s_planes[sb * PT + tid] : 0ull;  // above warp_w: zero
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int p = 8 * sb + k;
+            if (p < w) {
+                const uint32_t byte = (uint32_t)(y >> (8 * k)) & 0xffu;
+                uint8_t* row = s_stage + s_rowoff[p];
+                if ((dense >> p) & 1) {
+                    if (active) row[tid] = (uint8_t)byte;
+                } else {
+                    // bitmap: byte j nonzero -> bit 7-j%8 of bitmap byte j/8; then the
+                    // nonzero bytes in order (bitplane.hpp:126-148)
+                    const uint32_t m = __ballot_sync(0xffffffffu, byte != 0);
+                    if ((lane & 7) == 0 && active) row[tid >> 3] = (uint8_t)(__brev(m >> lane) >> 24);
+                    if (byte) row[BM + s_wpre[p * 32 + warp] + __popc(m & lt_mask)] = (uint8_t)byte;
+                }
             }
         }
     }
     __syncthreads();
 
-    // ---- store: 16-B vectors for whole segments, bytes at the two ragged ends ----
-    uint8_t* dst = out + (off - a);
-    const uint32_t end = a + size;
-    const uint32_t nvec = (end + 15) >> 4;
-    for (uint32_t v = tid; v < nvec; v += blockDim.x) {
-        const uint32_t lo = v << 4, hi = lo + 16;
-        if (lo >= a && hi <= end) {
-            *reinterpret_cast<uint4*>(dst + lo) = *reinterpret_cast<const uint4*>(s_stage + lo);
-        } else {
-            const uint32_t from = lo > a ? lo : a, to = hi < end ? hi : end;
-            for (uint32_t i = from; i < to; ++i) dst[i] = s_stage[i];
-        }
-    }
+    // ---- store the image into this chunk's scratch slot (16-B aligned) ----
+    uint4* dst = reinterpret_cast<uint4*>(ws.images + c * (uint64_t)ws.slot);
+    const uint4* srcv = reinterpret_cast<const uint4*>(s_stage);
+    const uint32_t nvec = (size + 15) >> 4;
+    for (uint32_t vv = tid; vv < nvec; vv += blockDim.x) dst[vv] = srcv[vv];
 }
 
-// Batch tables + header (container.cpp:44-55, 88-111).  Every chunk's inclusive
-// prefix is final once encode_chunks_kernel has returned.
-__global__ void frame_tables_kernel(geometry g, uint8_t* __restrict__ out, uint64_t out_cap,
-                                    encode_ws ws, archive_header_bytes hdr) {
-    const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c == 0 && g.header_bytes == 47) {
+// Placement: chunk images -> archive.  A tile of kPlaceTile consecutive chunks per CTA;
+// sizes are known up front, so every tile publishes its aggregate at once and the
+// decoupled look-back never waits on compute.  The tile then writes its chunks'
+// size-table entries (container.cpp:88-111), copies each image to
+// chunk_base(c) + exclusive prefix with funnel-shifted 16-B stores, and the first
+// tile writes the 47-byte header (container.cpp:44-55).
+__global__ void __launch_bounds__(kPlaceTile) place_chunks_kernel(geometry g, uint8_t* __restrict__ out,
+                                                                  uint64_t out_cap, encode_ws ws,
+                                                                  archive_header_bytes hdr) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kPlaceTile / 32;
+    __shared__ uint32_t s_ticket;
+    __shared__ uint32_t s_wsum[NW];
+    __shared__ uint64_t s_tile_excl;
+    __shared__ uint64_t s_off[kPlaceTile];
+    __shared__ uint32_t s_sz[kPlaceTile];
+    if (tid == 0) s_ticket = atomicAdd(ws.ticket, 1u);
+    __syncthreads();
+    const uint64_t t = s_ticket;
+    const uint64_t c = t * kPlaceTile + tid;
+    const bool valid = c < g.n_chunks;
+    const uint32_t sz = valid ? ws.sizes[c] : 0u;
+
+    // tile-local exclusive scan (a tile holds < 2^32 bytes)
+    uint32_t incl = sz;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += x;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    uint32_t wbase = 0, tile_sum = 0;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {
+        wbase += q < warp ? s_wsum[q] : 0u;
+        tile_sum += s_wsum[q];
+    }
+    // decoupled look-back over tiles (warp 0)
+    if (warp == 0) {
+        uint64_t excl = 0;
+        if (lane == 0) st_relaxed(&ws.tile_status[t], (t == 0 ? kFlagInc : kFlagAgg) | tile_sum);
+        if (t > 0) {
+            int64_t j = (int64_t)t - 1;
+            for (;;) {
+                const int64_t idx = j - lane;
+                uint64_t st = idx >= 0 ? ld_relaxed(&ws.tile_status[idx]) : kFlagInc;
+                uint32_t inc, need;
+                for (;;) {
+                    inc = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+                    const uint32_t ready = __ballot_sync(0xffffffffu, (st >> 62) != 0);
+                    need = inc ? (0xffffffffu >> (32 - __ffs(inc))) : 0xffffffffu;
+                    if ((ready & need) == need) break;
+                    __nanosleep(32);
+                    if ((st >> 62) == 0) st = ld_relaxed(&ws.tile_status[idx]);
+                }
+                excl += warp_sum_u64(((need >> lane) & 1) ? (st & kValMask) : 0);
+                if (inc) break;
+                j -= 32;
+            }
+            if (lane == 0) st_relaxed(&ws.tile_status[t], kFlagInc | (excl + tile_sum));
+        }
+        if (lane == 0) s_tile_excl = excl;
+    }
+    __syncthreads();
+    const uint64_t pexcl = s_tile_excl + wbase + (incl - sz);  // payload bytes before chunk c
+    s_off[tid] = valid ? g.chunk_base(c) + pexcl : 0;
+    s_sz[tid] = sz;
+
+    if (valid) {
+        const uint64_t b = g.batch_of(c);
+        if (c == b * g.cpb) {  // first chunk of its batch: publish the batch payload prefix
+            __threadfence();
+            st_relaxed(&ws.batch_prefix[b], (1ull << 63) | pexcl);
+        }
+    }
+    __syncthreads();
+    if (valid) {
+        const uint64_t b = g.batch_of(c);
+        const uint32_t ci = (uint32_t)(c - b * g.cpb);
+        const uint64_t first = b * g.cpb;
+        uint64_t pf;
+        if (first >= t * kPlaceTile) {
+            pf = s_off[first - t * kPlaceTile] - g.chunk_base(first);
+        } else {
+            uint64_t w8;
+            while (((w8 = ld_relaxed(&ws.batch_prefix[b])) >> 63) == 0) __nanosleep(64);
+            pf = w8 & ~(1ull << 63);
+        }
+        const uint64_t frame = g.frame_base(b) + pf;
+        if (frame + 4 + 4 * (uint64_t)g.chunks_in(b) <= out_cap) {
+            uint8_t* e = out + frame + 4 + 4 * (uint64_t)ci;
+            e[0] = (uint8_t)sz;
+            e[1] = (uint8_t)(sz >> 8);
+            e[2] = (uint8_t)(sz >> 16);
+            e[3] = (uint8_t)(sz >> 24);
+            if (ci == 0) {
+                const uint32_t cnt = g.chunks_in(b);
+                out[frame] = (uint8_t)cnt;
+                out[frame + 1] = (uint8_t)(cnt >> 8);
+                out[frame + 2] = (uint8_t)(cnt >> 16);
+                out[frame + 3] = (uint8_t)(cnt >> 24);
+            }
+        }
+        if (c + 1 == g.n_chunks) *ws.total = s_off[tid] + sz;
+    }
+    if (t == 0 && tid == 0 && g.header_bytes == 47) {
         for (int i = 0; i < 47; ++i) out[i] = hdr.b[i];
     }
-    if (c >= g.n_chunks) return;
-    const uint64_t inc = ws.status[c] & kValMask;
-    const uint64_t prev = c ? (ws.status[c - 1] & kValMask) : 0;
-    const uint64_t b = g.batch_of(c);
-    const uint32_t ci = (uint32_t)(c - b * g.cpb);
-    const uint64_t first = b * g.cpb;
-    const uint64_t pfirst = first ? (ws.status[first - 1] & kValMask) : 0;
-    const uint64_t frame = g.frame_base(b) + pfirst;
-    const uint32_t size = (uint32_t)(inc - prev);
-    if (frame + 4 + 4 * (uint64_t)g.chunks_in(b) > out_cap) return;  // capacity error already raised
-    uint8_t* e = out + frame + 4 + 4 * (uint64_t)ci;
-    e[0] = (uint8_t)size;
-    e[1] = (uint8_t)(size >> 8);
-    e[2] = (uint8_t)(size >> 16);
-    e[3] = (uint8_t)(size >> 24);
-    if (ci == 0) {
-        const uint32_t cnt = g.chunks_in(b);
-        out[frame] = (uint8_t)cnt;
-        out[frame + 1] = (uint8_t)(cnt >> 8);
-        out[frame + 2] = (uint8_t)(cnt >> 16);
-        out[frame + 3] = (uint8_t)(cnt >> 24);
+
+    // copy: each warp moves its 32 chunks, one after another
+    for (int k = 0; k < 32; ++k) {
+        const int idx = warp * 32 + k;
+        const uint64_t cc = t * kPlaceTile + idx;
+        if (cc >= g.n_chunks) break;
+        const uint64_t off = s_off[idx];
+        const uint32_t size = s_sz[idx];
+        if (off + size > out_cap) {
+            if (lane == 0) record_error(ws.error, cc, DEV_E_CAPACITY);
+            continue;
+        }
+        const uint32_t* img = reinterpret_cast<const uint32_t*>(ws.images + cc * (uint64_t)ws.slot);
+        const uint32_t a = (uint32_t)(off & 15);
+        uint8_t* dstb = out + (off - a);
+        const uint32_t end = a + size;
+        const uint32_t nvec = (end + 15) >> 4;
+        for (uint32_t vv = lane; vv < nvec; vv += 32) {
+            const uint32_t lo = vv << 4, hi = lo + 16;
+            if (lo >= a && hi <= end) {
+                // destination bytes [lo, lo+16) = image bytes [lo - a, lo - a + 16)
+                const uint32_t sb = lo - a;
+                const uint32_t w0 = sb >> 2, sh = (sb & 3) * 8;
+                uint32_t r[5];
+#pragma unroll
+                for (int i = 0; i < 5; ++i) r[i] = __ldg(img + w0 + i);
+                uint4 o;
+                o.x = __funnelshift_r(r[0], r[1], sh);
+                o.y = __funnelshift_r(r[1], r[2], sh);
+                o.z = __funnelshift_r(r[2], r[3], sh);
+                o.w = __funnelshift_r(r[3], r[4], sh);
+                *reinterpret_cast<uint4*>(dstb + lo) = o;
+            } else {
+                const uint8_t* ib = reinterpret_cast<const uint8_t*>(img);
+                const uint32_t from = lo > a ? lo : a, to = hi < end ? hi : end;
+                for (uint32_t i = from; i < to; ++i) dstb[i] = ib[i - a];
+            }
+        }
     }
-    if (c + 1 == g.n_chunks) *ws.total = g.chunk_base(c) + inc;
 }
 
 uint32_t encode_block_threads(uint32_t chunk_n) {
@@ -385,41 +507,93 @@ template <typename T>
 uint32_t encode_smem_bytes(uint32_t chunk_n) {
     using tr = lane_traits<T>;
     const uint32_t nc = (chunk_n - 1) / 8;
-    // staging for the largest chunk image plus its 16-B phase shares the values region
-    const uint32_t vals = encode_region_bytes<T>(chunk_n);
-    const uint32_t rows = (tr::width * nc + 15) & ~15u;
-    const uint32_t nzw = tr::width * (encode_block_threads(chunk_n) / 32) * 2;
-    return vals + rows + nzw;
+    (void)nc;
+    return encode_stage_bytes<T>(chunk_n) + (tr::width / 8) * encode_block_threads(chunk_n) * 8;
+}
+
+template <typename T>
+uint32_t encode_slot_bytes(uint32_t chunk_n) {
+    // max_encoded_chunk_size (chunk_codec.hpp:36-41) + 4 readable bytes for the funnel
+    // loads of the placement copy, rounded to 16
+    using tr = lane_traits<T>;
+    const uint32_t nc = (chunk_n - 1) / 8;
+    return (uint32_t)(tr::header + (tr::width + 7) / 8 + tr::width * nc + 4 + 15) & ~15u;
+}
+
+template <typename T>
+size_t encode_scratch_bytes(const geometry& g) {
+    const uint64_t tiles = (g.n_chunks + kPlaceTile - 1) / kPlaceTile;
+    size_t b = 0;
+    b += (g.n_chunks * 4 + 15) & ~15ull;                 // sizes
+    b += tiles * 8;                                       // tile status
+    b += (g.n_batches + 1) * 8;                           // batch prefixes
+    b = (b + 255) & ~255ull;
+    b += g.n_chunks * (uint64_t)encode_slot_bytes<T>(g.chunk_n);  // images
+    return b;
+}
+
+template <typename T>
+encode_ws carve_encode_ws(void* scratch, const geometry& g, uint32_t* ticket, unsigned long long* error,
+                          uint64_t* total) {
+    encode_ws ws;
+    uint8_t* p = static_cast<uint8_t*>(scratch);
+    const uint64_t tiles = (g.n_chunks + kPlaceTile - 1) / kPlaceTile;
+    ws.sizes = reinterpret_cast<uint32_t*>(p);
+    p += (g.n_chunks * 4 + 15) & ~15ull;
+    ws.tile_status = reinterpret_cast<uint64_t*>(p);
+    p += tiles * 8;
+    ws.batch_prefix = reinterpret_cast<uint64_t*>(p);
+    p += (g.n_batches + 1) * 8;
+    const size_t used = (size_t)(p - static_cast<uint8_t*>(scratch));
+    p = static_cast<uint8_t*>(scratch) + ((used + 255) & ~255ull);
+    ws.images = p;
+    ws.slot = encode_slot_bytes<T>(g.chunk_n);
+    ws.ticket = ticket;
+    ws.error = error;
+    ws.total = total;
+    return ws;
 }
 
 template <typename T>
 cudaError_t launch_encode(const T* d_in, const geometry& g, uint8_t* d_out, uint64_t out_cap,
-                          const encode_ws& ws, const archive_header_bytes& hdr, cudaStream_t st) {
+                          const encode_ws& ws, const archive_header_bytes& hdr, cudaStream_t st,
+                          cudaEvent_t ev0, cudaEvent_t ev1) {
     cudaError_t e;
-    if ((e = cudaMemsetAsync(ws.status, 0, g.n_chunks * sizeof(uint64_t), st))) return e;
-    if ((e = cudaMemsetAsync(ws.ticket, 0, sizeof(uint32_t), st))) return e;
     if (g.n_chunks == 0) {
         // empty input: a bare header (test_pipeline.cpp:109-122)
         if ((e = cudaMemcpyAsync(ws.total, &g.header_bytes, sizeof(uint64_t), cudaMemcpyHostToDevice, st)))
             return e;
         return g.header_bytes ? cudaMemcpyAsync(d_out, hdr.b, 47, cudaMemcpyHostToDevice, st) : cudaSuccess;
     }
+    const uint64_t tiles = (g.n_chunks + kPlaceTile - 1) / kPlaceTile;
+    // tile status + batch prefixes are contiguous
+    if ((e = cudaMemsetAsync(ws.tile_status, 0, (tiles + g.n_batches + 1) * 8, st))) return e;
+    if ((e = cudaMemsetAsync(ws.ticket, 0, sizeof(uint32_t), st))) return e;
     const uint32_t threads = encode_block_threads(g.chunk_n);
     const uint32_t smem = encode_smem_bytes<T>(g.chunk_n);
     auto kern = threads <= 256 ? encode_chunks_kernel<T, 256> : encode_chunks_kernel<T, 1024>;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    if (ev0 && (e = cudaEventRecord(ev0, st))) return e;
     kern<<<(unsigned)g.n_chunks, threads, smem, st>>>(d_in, g, d_out, out_cap, ws);
     if ((e = cudaGetLastError())) return e;
-    const unsigned tb = 256;
-    frame_tables_kernel<<<(unsigned)((g.n_chunks + tb - 1) / tb), tb, 0, st>>>(g, d_out, out_cap, ws, hdr);
+    if (ev1 && (e = cudaEventRecord(ev1, st))) return e;
+    place_chunks_kernel<<<(unsigned)tiles, kPlaceTile, 0, st>>>(g, d_out, out_cap, ws, hdr);
     return cudaGetLastError();
 }
 
 template cudaError_t launch_encode<double>(const double*, const geometry&, uint8_t*, uint64_t,
-                                           const encode_ws&, const archive_header_bytes&, cudaStream_t);
+                                           const encode_ws&, const archive_header_bytes&, cudaStream_t,
+                                           cudaEvent_t, cudaEvent_t);
 template cudaError_t launch_encode<float>(const float*, const geometry&, uint8_t*, uint64_t,
-                                          const encode_ws&, const archive_header_bytes&, cudaStream_t);
+                                          const encode_ws&, const archive_header_bytes&, cudaStream_t,
+                                          cudaEvent_t, cudaEvent_t);
 template uint32_t encode_smem_bytes<double>(uint32_t);
 template uint32_t encode_smem_bytes<float>(uint32_t);
+template uint32_t encode_slot_bytes<double>(uint32_t);
+template uint32_t encode_slot_bytes<float>(uint32_t);
+template size_t encode_scratch_bytes<double>(const geometry&);
+template size_t encode_scratch_bytes<float>(const geometry&);
+template encode_ws carve_encode_ws<double>(void*, const geometry&, uint32_t*, unsigned long long*, uint64_t*);
+template encode_ws carve_encode_ws<float>(void*, const geometry&, uint32_t*, unsigned long long*, uint64_t*);
 
 }  // namespace fb200

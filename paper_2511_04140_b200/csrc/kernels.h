@@ -12,13 +12,25 @@ struct archive_header_bytes {
     uint8_t b[48];
 };
 
-// Scratch for one compress launch (device memory, owned by the context).
+// Scratch for one compress launch (device memory, owned by the caller/context).
+// Carved out of one buffer by carve_encode_ws(); encode_scratch_bytes() sizes it.
 struct encode_ws {
-    uint64_t* status;             // [n_chunks] look-back words: flag(2b) | value(62b)
-    uint32_t* ticket;             // CTA ticket counter (chunk order)
+    uint8_t* images;              // [n_chunks][slot] chunk images (16-B aligned slots)
+    uint32_t slot;                // bytes per image slot
+    uint32_t* sizes;              // [n_chunks] encoded chunk sizes
+    uint64_t* tile_status;        // [n_tiles] placement look-back words
+    uint64_t* batch_prefix;       // [n_batches] payload prefix of each batch | ready bit
+    uint32_t* ticket;             // placement tile ticket counter
     unsigned long long* error;    // (chunk << 8 | code), ~0 = none
-    uint64_t* total;              // archive bytes, written by frame_tables_kernel
+    uint64_t* total;              // archive bytes, written by the placement kernel
 };
+
+constexpr uint32_t kPlaceTile = 256;  // chunks per placement tile
+template <typename T> uint32_t encode_slot_bytes(uint32_t chunk_n);
+template <typename T> size_t encode_scratch_bytes(const geometry& g);
+template <typename T>
+encode_ws carve_encode_ws(void* scratch, const geometry& g, uint32_t* ticket,
+                          unsigned long long* error, uint64_t* total);
 
 // Scratch for one decompress launch.
 struct decode_ws {
@@ -34,14 +46,20 @@ uint32_t encode_block_threads(uint32_t chunk_n);
 template <typename T> uint32_t encode_smem_bytes(uint32_t chunk_n);
 template <typename T> uint32_t decode_smem_bytes(uint32_t chunk_n);
 
+// ev0/ev1 (optional) are recorded right before / after the main kernel (profiling hook).
 template <typename T>
 cudaError_t launch_encode(const T* d_in, const geometry& g, uint8_t* d_out, uint64_t out_cap,
-                          const encode_ws& ws, const archive_header_bytes& hdr, cudaStream_t st);
+                          const encode_ws& ws, const archive_header_bytes& hdr, cudaStream_t st,
+                          cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 
 // d_archive points at the archive's first byte (the 47-byte header), `len` bytes long.
 template <typename T>
 cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry& g, T* d_out,
-                          const decode_ws& ws, cudaStream_t st);
+                          const decode_ws& ws, cudaStream_t st, cudaEvent_t ev0 = nullptr,
+                          cudaEvent_t ev1 = nullptr);
+
+cudaError_t launch_selftest_dp(int prec, const void* v, uint64_t n, int A, int8_t* full,
+                               int8_t* lit, int8_t* cert, int64_t* g, cudaStream_t st);
 
 // One-time upload of the pow10 / decade tables (numeric.hpp:17-41, numeric.cpp:10-39).
 cudaError_t upload_tables();

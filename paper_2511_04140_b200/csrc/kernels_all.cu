@@ -4,3 +4,4 @@
 #include "tables.cu"
 #include "encode.cu"
 #include "decode.cu"
+#include "selftest.cu"

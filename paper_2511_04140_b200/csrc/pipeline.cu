@@ -146,7 +146,7 @@ falcon_status run_compress(falcon_ctx* ctx, int prec, compress_io& io,
         const uint64_t fbound = frame_bound(prec, s.count, chunk_n);
         FB_TRY(s.d_in.ensure(s.count * esz));
         FB_TRY(s.d_out.ensure(fbound));
-        FB_TRY(s.d_status.ensure(g.n_chunks * 8 + 8));
+        FB_TRY(s.d_status.ensure(prec == FALCON_F64 ? encode_scratch_bytes<double>(g) : encode_scratch_bytes<float>(g)));
         const uint8_t* h_src = stage_ptr;
         if (!direct_in) {
             // swap the staged buffer into the slot (pipeline.hpp:281 s.input.swap(stage))
@@ -158,8 +158,11 @@ falcon_status run_compress(falcon_ctx* ctx, int prec, compress_io& io,
         FB_CUDA(cudaMemcpyAsync(s.d_in.p, h_src, s.count * esz, cudaMemcpyHostToDevice, st));
         uint8_t* misc = s.d_misc.as<uint8_t>();
         FB_CUDA(cudaMemsetAsync(misc + 8, 0xff, 8, st));
-        encode_ws ws{s.d_status.as<uint64_t>(), reinterpret_cast<uint32_t*>(misc),
-                     reinterpret_cast<unsigned long long*>(misc + 8), reinterpret_cast<uint64_t*>(misc + 16)};
+        auto* err = reinterpret_cast<unsigned long long*>(misc + 8);
+        auto* tot = reinterpret_cast<uint64_t*>(misc + 16);
+        const encode_ws ws = prec == FALCON_F64
+                                 ? carve_encode_ws<double>(s.d_status.p, g, reinterpret_cast<uint32_t*>(misc), err, tot)
+                                 : carve_encode_ws<float>(s.d_status.p, g, reinterpret_cast<uint32_t*>(misc), err, tot);
         const archive_header_bytes none{};
         cudaError_t e = prec == FALCON_F64
                             ? launch_encode<double>(s.d_in.as<double>(), g, s.d_out.as<uint8_t>(), fbound, ws, none, st)

@@ -156,5 +156,6 @@ struct falcon_ctx {
     unsigned pool_workers = 0;
     std::mutex api_mutex;           // one API call at a time per context
     uint64_t last_archive_bytes = 0;
+    cudaEvent_t prof_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // encode / decode kernel brackets
     fb200::worker_pool& get_pool(unsigned workers);
 };

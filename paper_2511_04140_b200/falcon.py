@@ -28,6 +28,7 @@ EXPORTED = [
     "falcon_compress_device_async", "falcon_decompress_device", "falcon_decompress_device_async",
     "falcon_ctx_sync", "falcon_compress_stream", "falcon_decompress_stream", "falcon_compress_host",
     "falcon_decompress_host", "falcon_compress_chunk", "falcon_decompress_chunk", "falcon_synth_fill",
+    "falcon_ctx_set_kernel_events", "falcon_selftest_dp",
 ]
 
 
@@ -100,6 +101,8 @@ def load() -> C.CDLL:
     L.falcon_decompress_device.argtypes = [vp, i32, vp, u64, vp, u64, C.POINTER(u64), vp]
     L.falcon_decompress_device_async.argtypes = [vp, i32, vp, u64, C.POINTER(ArchiveInfo), vp, u64, vp]
     L.falcon_ctx_sync.argtypes = [vp, vp]
+    L.falcon_ctx_set_kernel_events.argtypes = [vp, vp, vp, vp, vp]
+    L.falcon_selftest_dp.argtypes = [vp, i32, vp, u64, i32, vp, vp, vp, vp, vp]
     L.falcon_compress_stream.argtypes = [vp, i32, READ_FN, vp, STORE_FN, vp,
                                          C.POINTER(PipelineOptions), C.POINTER(PipelineStats)]
     L.falcon_decompress_stream.argtypes = [vp, i32, vp, u64, PUT_FN, vp, C.POINTER(PipelineOptions),
@@ -238,6 +241,28 @@ class Codec:
         _check(self.lib.falcon_decompress_device_async(
             self.ctx, prec_of(out.dtype), C.c_void_p(archive.data_ptr()), nbytes, C.byref(info),
             C.c_void_p(out.data_ptr()), out.numel(), st))
+
+    def set_kernel_events(self, enc=None, dec=None):
+        """enc/dec: (start, stop) torch.cuda.Event pairs recorded around the main kernels."""
+        h = lambda e: C.c_void_p(e.cuda_event) if e is not None else None  # noqa: E731
+        e0, e1 = enc if enc else (None, None)
+        d0, d1 = dec if dec else (None, None)
+        _check(self.lib.falcon_ctx_set_kernel_events(self.ctx, h(e0), h(e1), h(d0), h(d1)))
+
+    def selftest_dp(self, values, candidate_alpha: int):
+        """values: CUDA tensor.  Returns (full, literal, cert, g) CPU numpy arrays."""
+        import torch
+        n = values.numel()
+        dev_ = values.device
+        f = torch.empty(n, dtype=torch.int8, device=dev_)
+        lit = torch.empty(n, dtype=torch.int8, device=dev_)
+        c = torch.empty(n, dtype=torch.int8, device=dev_)
+        g = torch.empty(n, dtype=torch.int64, device=dev_)
+        st = C.c_void_p(torch.cuda.current_stream(dev_).cuda_stream)
+        _check(self.lib.falcon_selftest_dp(self.ctx, prec_of(values.dtype), C.c_void_p(values.data_ptr()), n,
+                                           candidate_alpha, C.c_void_p(f.data_ptr()), C.c_void_p(lit.data_ptr()),
+                                           C.c_void_p(c.data_ptr()), C.c_void_p(g.data_ptr()), st))
+        return f.cpu().numpy(), lit.cpu().numpy(), c.cpu().numpy(), g.cpu().numpy()
 
     def sync(self, stream=None):
         import torch
