@@ -24,6 +24,8 @@
 //     gives the same verdict.  When the test fails at A nothing is concluded.
 #pragma once
 
+#include <climits>
+
 #include "falcon_common.cuh"
 
 namespace fb200 {
@@ -138,6 +140,81 @@ __device__ __noinline__ int dp_alpha_full(T v) {
 }
 
 enum : int { CERT_UNDECIDED = 0, CERT_OK = 1, CERT_EXC = 2 };
+
+// Branch-free form of dp_certify for the encoder's hot loop: same verdicts (the
+// self-test compares the two), written with selects so the unrolled per-thread
+// values interleave.  Also returns floor_log10(|v|) of nonzero normal values
+// (max over the chunk gives floor_log10(max|v|) for beta_hat, transform.hpp:62-63);
+// *mag = INT_MIN for zeros and specials.
+__device__ __forceinline__ int certify_fast(double v, int A, double p, int64_t* g, int* mag_out) {
+    using X = fpx<double>;
+    const uint64_t b = X::bits(v);
+    const uint32_t hi = (uint32_t)(b >> 32), lo = (uint32_t)b;
+    const uint32_t ahi = hi & 0x7fffffffu;
+    const bool zero = (ahi | lo) == 0;
+    const uint32_t ef = ahi >> 20;
+    const bool special = ef == 0 || ef == 0x7ffu;
+    const int e2 = (int)ef - 1023;
+    const int k0 = (e2 * 78913) >> 18;
+    const int ki = k0 + 1 < 308 ? k0 + 1 : 308;
+    const int mag = k0 + ((b & ~X::SIGN) >= X::dec(ki) ? 1 : 0);
+    const bool inrange = A + mag >= 0 && A + mag <= X::MAXB - 1;
+    // gap test: |s - rint(s)| <= ulp(s)  (valid for |s| >= 1/2, guaranteed when inrange)
+    const double s = __dmul_rn(v, p);
+    const double r = rint(s);
+    const double d = __dsub_rn(s, r);
+    const uint32_t uhi = (__double2hiint(s) & 0x7ff00000u) - (52u << 20);
+    const double ulp = __hiloint2double((int)uhi, 0);
+    const bool near = fabs(d) <= ulp;
+    // reconstruction: |N - v*p| against p * ulp(v) / 2, halved below a power of two
+    const double e = __fma_rn(-v, p, r);
+    const bool toward0 = (__double2hiint(e) ^ (int)hi) < 0;
+    const bool pow2 = (hi & 0x000fffffu) == 0 && lo == 0;
+    const uint32_t hexp = ef - 53u - ((pow2 && toward0) ? 1u : 0u);
+    const double H = __dmul_rn(p, __hiloint2double((int)(hexp << 20), 0));
+    const double ae = fabs(e);
+    const bool recon = ae < H || (ae == H && (lo & 1u) == 0);
+    *g = zero ? 0 : (int64_t)__double2ll_rz(r);
+    *mag_out = (zero || special) ? INT_MIN : mag;
+    if (zero) return (hi >> 31) ? CERT_EXC : CERT_OK;
+    if (special) return CERT_EXC;
+    if (!inrange || !near) return CERT_UNDECIDED;
+    return recon ? CERT_OK : CERT_EXC;
+}
+
+__device__ __forceinline__ int certify_fast(float v, int A, float p, int32_t* g, int* mag_out) {
+    using X = fpx<float>;
+    const uint32_t b = X::bits(v);
+    const uint32_t ab = b & 0x7fffffffu;
+    const bool zero = ab == 0;
+    const uint32_t ef = ab >> 23;
+    const bool special = ef == 0 || ef == 0xffu;
+    const int e2 = (int)ef - 127;
+    const int k0 = (e2 * 78913) >> 18;
+    const int ki = k0 + 1 < 38 ? k0 + 1 : 38;
+    const int mag = k0 + (ab >= X::dec(ki) ? 1 : 0);
+    const bool inrange = A + mag >= 0 && A + mag <= X::MAXB - 1;
+    const float s = __fmul_rn(v, p);
+    const float r = rintf(s);
+    const float d = __fsub_rn(s, r);
+    const float ulp = __uint_as_float((__float_as_uint(s) & 0x7f800000u) - (23u << 23));
+    const bool near = fabsf(d) <= ulp;
+    const double e = __fma_rn(-(double)v, (double)p, (double)r);
+    const bool toward0 = ((uint32_t)__double2hiint(e) >> 31) != (b >> 31);
+    const bool pow2 = (b & 0x007fffffu) == 0;
+    // 2^(ev - 24) as a double: exponent field ef - 127 - 24 + 1023
+    const uint32_t hexp = ef + 872u - ((pow2 && toward0) ? 1u : 0u);
+    const double H = __dmul_rn((double)p, __hiloint2double((int)(hexp << 20), 0));
+    const double ae = fabs(e);
+    const bool recon = ae < H || (ae == H && (b & 1u) == 0);
+    *g = zero ? 0 : (int32_t)__float2int_rz(r);
+    *mag_out = (zero || special) ? INT_MIN : mag;
+    if (zero) return (b >> 31) ? CERT_EXC : CERT_OK;
+    if (special) return CERT_EXC;
+    if (!inrange || !near) return CERT_UNDECIDED;
+    return recon ? CERT_OK : CERT_EXC;
+}
+
 
 // (3): decide v against candidate scale A (0 <= A <= max_alpha).  CERT_OK: alpha_v <= A
 // and v is not an exception, *g = round_half_away(v*10^A).  CERT_EXC: v is an

@@ -75,6 +75,15 @@ __host__ __device__ __forceinline__ uint32_t encode_stage_bytes(uint32_t chunk_n
     return (uint32_t)(tr::header + (tr::width + 7) / 8 + tr::width * nc + 32 + 15) & ~15u;
 }
 
+// 32-bit word of lane values whose byte q is gathered (sb < 4: low word, else high)
+__device__ __forceinline__ uint32_t lane_word(uint64_t z, int sb) { return sb < 4 ? (uint32_t)z : (uint32_t)(z >> 32); }
+__device__ __forceinline__ uint32_t lane_word(uint32_t z, int) { return z; }
+
+// 0x01 in every nonzero byte of w
+__device__ __forceinline__ uint32_t nonzero_bytes(uint32_t w) {
+    return ((((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w) >> 7) & 0x01010101u;
+}
+
 template <typename T, int MAXT>
 __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1)
     encode_chunks_kernel(const T* __restrict__ in, geometry g, uint8_t* __restrict__ out,
@@ -91,15 +100,15 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1)
     const int BM = NC / 8;              // sparse bitmap bytes
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = blockDim.x >> 5;
-
-    uint8_t* s_stage = smem;                                  // chunk image
-    // [block][thread] u64: byte k of entry (s, t) = row byte t of bit plane 8s+k
-    uint64_t* s_planes = reinterpret_cast<uint64_t*>(smem + encode_stage_bytes<T>(n));
     const int PT = (int)blockDim.x;
 
-    __shared__ int s_a0[32], s_amax[32];
-    __shared__ uint32_t s_exc[32], s_warpw[32];
-    __shared__ B s_vmax[32];
+    uint8_t* s_stage = smem;  // chunk image (phase 0)
+    // [block][thread] u64: byte k of entry (s, t) = row byte t of bit plane 8s+k
+    uint64_t* s_planes = reinterpret_cast<uint64_t*>(smem + encode_stage_bytes<T>(n));
+
+    __shared__ uint32_t s_flag1[32], s_flag2[32];  // per warp: bit 31 exception | one-hot alphas
+    __shared__ uint32_t s_mag[32];                 // per warp: max floor_log10 + 1024 (0: none)
+    __shared__ uint32_t s_warpw[32];
     __shared__ uint32_t s_rowoff[64];
     __shared__ uint32_t s_nzc[32][16];   // per warp: 8-bit nonzero-byte counters, 4 planes/word
     __shared__ uint16_t s_wpre[64 * 32]; // nonzero bytes of plane p in warps before w
@@ -126,79 +135,79 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1)
         for (int j = 0; j < 8; ++j) v[j] = (active && i0 + 1 + j < len) ? __ldg(src + i0 + 1 + j) : T(0);
         if (active && i0 < len) vprev = __ldg(src + i0);
     }
+    // the image is built on a zeroed buffer: zero bytes are never written
+    {
+        uint4* st = reinterpret_cast<uint4*>(s_stage);
+        const int words = (int)(encode_stage_bytes<T>(n) >> 4);
+        for (int i = tid; i < words; i += PT) st[i] = make_uint4(0u, 0u, 0u, 0u);
+    }
 
     // ---- analyze, phase 1: exact loop on one sample per thread -> A0 ----
-    int a1 = active ? dp_alpha_full<T>(v[0]) : 0;
+    uint32_t f1 = 0;
+    if (active) {
+        const int a = dp_alpha_full<T>(v[0]);
+        f1 = a < 0 ? 0x80000000u : (1u << a);
+    }
     if (tid == 0) {  // value 0 is analysed by thread 0 only
-        const int az = dp_alpha_full<T>(vprev);
-        a1 = (a1 < 0 || az < 0) ? -1 : (az > a1 ? az : a1);
+        const int a = dp_alpha_full<T>(vprev);
+        f1 |= a < 0 ? 0x80000000u : (1u << a);
     }
-    {
-        const bool we = __any_sync(0xffffffffu, a1 < 0);
-        const int wa = (int)__reduce_max_sync(0xffffffffu, (uint32_t)(a1 < 0 ? 0 : a1));
-        if (lane == 0) {
-            s_a0[warp] = wa;
-            s_exc[warp] = we;
-        }
-    }
+    f1 = __reduce_or_sync(0xffffffffu, f1);
+    if (lane == 0) s_flag1[warp] = f1;
     __syncthreads();
-    int A0 = 0;
-    bool exc = false;
-    for (int i = 0; i < nwarps; ++i) {
-        A0 = s_a0[i] > A0 ? s_a0[i] : A0;
-        exc |= s_exc[i] != 0;
-    }
+    uint32_t F = 0;
+    for (int i = 0; i < nwarps; ++i) F |= s_flag1[i];
+    const int A0 = (F & 0x7fffffffu) ? 31 - __clz((int)(F & 0x7fffffffu)) : 0;
 
-    // ---- analyze, phase 2: certify every value against A0 ----
+    // ---- analyze, phase 2: certify every value against A0 (dpds.cuh (3)) ----
     const T pA0 = X::pow10(A0);
     S gc[8];
-    uint32_t redo = 0;  // lanes whose lane integer must be recomputed at alpha_max
-    int afb = A0;       // max over values decided by the exact loop
-    B vmax = 0;
-    if (active) {
+    uint32_t redo = 0;   // lanes whose lane integer must be recomputed at alpha_max
+    uint32_t f2 = 0;     // exception bit | one-hot alphas of values decided by the exact loop
+    int magmax = INT_MIN;
+    if (active && !(F >> 31)) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const B mb = X::bits(v[j]) & ~X::SIGN;
-            vmax = mb > vmax ? mb : vmax;
-            gc[j] = 0;
-            if (exc) continue;  // the chunk already takes the raw path
-            const int r = dp_certify<T>(v[j], A0, pA0, &gc[j]);
-            if (r == CERT_EXC) {
-                exc = true;
-            } else if (r == CERT_UNDECIDED) {
-                redo |= 1u << j;
-                const int av = dp_alpha_full<T>(v[j]);
-                if (av < 0) exc = true;
-                else afb = av > afb ? av : afb;
+            int mg;
+            const int r = certify_fast(v[j], A0, pA0, &gc[j], &mg);
+            magmax = mg > magmax ? mg : magmax;
+            f2 |= r == CERT_EXC ? 0x80000000u : 0u;
+            redo |= r == CERT_UNDECIDED ? (1u << j) : 0u;
+        }
+        for (uint32_t rest = redo; rest; rest &= rest - 1) {  // rare: exact loop
+            const int j = __ffs(rest) - 1;
+            T vj = v[0];
+#pragma unroll
+            for (int q = 1; q < 8; ++q) vj = j == q ? v[q] : vj;
+            const int a = dp_alpha_full<T>(vj);
+            f2 |= a < 0 ? 0x80000000u : (1u << a);
+        }
+        if (tid == 0) {  // floor_log10 of value 0 for beta_hat
+            const B mb = X::bits(vprev) & ~X::SIGN;
+            const B ef = mb & X::EXPF;
+            if (mb != 0 && ef != 0 && ef != X::EXPF) {
+                const int mg = mag_of<T>(mb);
+                magmax = mg > magmax ? mg : magmax;
             }
         }
-        if (tid == 0) {
-            const B mb = X::bits(vprev) & ~X::SIGN;
-            vmax = mb > vmax ? mb : vmax;
-        }
     }
-    {
-        const bool we = __any_sync(0xffffffffu, exc);
-        const int wa = (int)__reduce_max_sync(0xffffffffu, (uint32_t)afb);
-        const B wv = warp_max<B>(vmax);
-        if (lane == 0) {
-            s_amax[warp] = wa;
-            s_exc[warp] = we;
-            s_vmax[warp] = wv;
-        }
+    f2 = __reduce_or_sync(0xffffffffu, f2);
+    const uint32_t mgw = __reduce_max_sync(0xffffffffu, magmax == INT_MIN ? 0u : (uint32_t)(magmax + 1024));
+    if (lane == 0) {
+        s_flag2[warp] = f2;
+        s_mag[warp] = mgw;
     }
     __syncthreads();
-    int amax = A0;
-    vmax = 0;
+    uint32_t M = 0;
     for (int i = 0; i < nwarps; ++i) {
-        amax = s_amax[i] > amax ? s_amax[i] : amax;
-        exc |= s_exc[i] != 0;
-        vmax = s_vmax[i] > vmax ? s_vmax[i] : vmax;
+        F |= s_flag2[i];
+        M = s_mag[i] > M ? s_mag[i] : M;
     }
-    bool case2 = exc;
+    const int amax = (F & 0x7fffffffu) ? 31 - __clz((int)(F & 0x7fffffffu)) : 0;
+    bool case2 = (F >> 31) != 0;
     int bhat = 0;
-    if (!case2) {  // transform.hpp:62-65
-        bhat = vmax == 0 ? 0 : amax + floor_log10_bits(vmax) + 1;
+    if (!case2) {  // transform.hpp:62-65; floor_log10(max|v|) = max floor_log10(|v|)
+        bhat = M == 0 ? 0 : amax + ((int)M - 1024) + 1;
         case2 = amax > tr::max_alpha || bhat > tr::max_beta;
     }
     const uint32_t hA = case2 ? tr::exc_alpha : (uint32_t)amax;
@@ -233,16 +242,19 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1)
     const int warp_w = bit_width(warp_or<B>(orv));
     const int nblk = (warp_w + 7) >> 3;
     for (int sb = 0; sb < nblk; ++sb) {
-        // lane j's byte sb at byte (7-j): byte k of the transpose is the row byte of bit
-        // plane 8sb+k with lane j at bit 7-j (MSB-first, FORMAT.md:81-84)
-        uint64_t x = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x |= (uint64_t)byte_of(z[j], sb) << (8 * (7 - j));
-        const uint64_t y = transpose8x8(x);
+        // byte sb of lane j goes to byte 7-j of x: byte k of the transpose is then the row
+        // byte of bit plane 8sb+k with lane j at bit 7-j (MSB-first, FORMAT.md:81-84)
+        const uint32_t q = (uint32_t)(sb & 3);
+        const uint32_t sel = q | ((4u + q) << 4);
+        const uint32_t xl = __byte_perm(__byte_perm(lane_word(z[7], sb), lane_word(z[6], sb), sel),
+                                        __byte_perm(lane_word(z[5], sb), lane_word(z[4], sb), sel), 0x5410);
+        const uint32_t xh = __byte_perm(__byte_perm(lane_word(z[3], sb), lane_word(z[2], sb), sel),
+                                        __byte_perm(lane_word(z[1], sb), lane_word(z[0], sb), sel), 0x5410);
+        const uint64_t y = transpose8x8(((uint64_t)xh << 32) | xl);
         s_planes[sb * PT + tid] = y;
-        // nonzero bytes per plane, 8-bit counters (<= 32 per warp, no carries)
-        const uint32_t lo = __reduce_add_sync(0xffffffffu, __vcmpne4((uint32_t)y, 0u) & 0x01010101u);
-        const uint32_t hi = __reduce_add_sync(0xffffffffu, __vcmpne4((uint32_t)(y >> 32), 0u) & 0x01010101u);
+        // nonzero bytes per plane as 8-bit counters (<= 32 per warp, no carries)
+        const uint32_t lo = __reduce_add_sync(0xffffffffu, nonzero_bytes((uint32_t)y));
+        const uint32_t hi = __reduce_add_sync(0xffffffffu, nonzero_bytes((uint32_t)(y >> 32)));
         if (lane == 0) {
             s_nzc[warp][2 * sb] = lo;
             s_nzc[warp][2 * sb + 1] = hi;
@@ -305,17 +317,16 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1)
     const uint32_t size = s_size;
     const uint64_t dense = s_dense;
 
-    // ---- emit the chunk image into staging: every thread writes its column of every
-    //      row; sparse rows place their nonzero bytes by warp prefix + ballot rank ----
-    if (tid == 0) {
-        uint8_t* h = s_stage;
-        h[0] = (uint8_t)hA;
-        h[1] = (uint8_t)hB;
-        const B z1 = s_z1;
-#pragma unroll
-        for (int i = 0; i < (int)sizeof(B); ++i) h[2 + i] = (uint8_t)(z1 >> (8 * i));
-        h[2 + sizeof(B)] = (uint8_t)w;
-        for (int i = 0; i < fb; ++i) h[HDR + i] = (uint8_t)(dense >> (8 * (fb - 1 - i)));
+    // ---- emit the chunk image: header bytes one per thread, then every thread writes
+    //      its column of every row (sparse rows: warp prefix + ballot rank) ----
+    if (tid < HDR + fb) {
+        uint32_t hb;
+        if (tid == 0) hb = hA;
+        else if (tid == 1) hb = hB;
+        else if (tid < 2 + (int)sizeof(B)) hb = (uint32_t)(s_z1 >> (8 * (tid - 2)));
+        else if (tid == 2 + (int)sizeof(B)) hb = (uint32_t)w;
+        else hb = (uint32_t)(dense >> (8 * (fb - 1 - (tid - HDR))));
+        s_stage[tid] = (uint8_t)hb;
     }
     const uint32_t lt_mask = (1u << lane) - 1u;
     const int wblk = (w + 7) >> 3;
@@ -328,13 +339,16 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1)
                 const uint32_t byte = (uint32_t)(y >> (8 * k)) & 0xffu;
                 uint8_t* row = s_stage + s_rowoff[p];
                 if ((dense >> p) & 1) {
-                    if (active) row[tid] = (uint8_t)byte;
+                    if (byte) row[tid] = (uint8_t)byte;
                 } else {
                     // bitmap: byte j nonzero -> bit 7-j%8 of bitmap byte j/8; then the
                     // nonzero bytes in order (bitplane.hpp:126-148)
                     const uint32_t m = __ballot_sync(0xffffffffu, byte != 0);
-                    if ((lane & 7) == 0 && active) row[tid >> 3] = (uint8_t)(__brev(m >> lane) >> 24);
-                    if (byte) row[BM + s_wpre[p * 32 + warp] + __popc(m & lt_mask)] = (uint8_t)byte;
+                    if (m) {
+                        const uint32_t bm8 = __brev(m >> lane) >> 24;
+                        if ((lane & 7) == 0 && (bm8 & 0xffu)) row[tid >> 3] = (uint8_t)bm8;
+                        if (byte) row[BM + s_wpre[p * 32 + warp] + __popc(m & lt_mask)] = (uint8_t)byte;
+                    }
                 }
             }
         }

@@ -4,6 +4,8 @@
 //   out_lit[i]  = literal reference loop         (dp_alpha: round(), IEEE division)
 //   out_cert[i] = dp_certify(v[i], A) code      (0 undecided, 1 ok, 2 exception)
 //   out_g[i]    = lane integer from certification (valid when code == 1)
+// and the branch-free encoder form certify_fast() must agree with dp_certify (code
+// 3 is written when they disagree, which the test treats as a failure).
 #include "dpds.cuh"
 #include "kernels.h"
 
@@ -18,7 +20,12 @@ __global__ void selftest_dp_kernel(const T* __restrict__ v, uint64_t n, int A, i
         out_full[i] = (int8_t)dp_alpha_full<T>(x);
         out_lit[i] = (int8_t)dp_alpha<T>(x);
         typename fpx<T>::S gv = 0;
-        out_cert[i] = (int8_t)dp_certify<T>(x, A, fpx<T>::pow10(A), &gv);
+        const T p = fpx<T>::pow10(A);
+        const int c1 = dp_certify<T>(x, A, p, &gv);
+        typename fpx<T>::S gf = 0;
+        int mg = 0;
+        const int c2 = certify_fast(x, A, p, &gf, &mg);
+        out_cert[i] = (int8_t)((c1 == c2 && (c1 != CERT_OK || gf == gv)) ? c1 : 3);
         out_g[i] = (int64_t)gv;
     }
 }

@@ -89,6 +89,7 @@ def test_fast_analysis_matches_oracle(codec, oracle, prec):
         assert len(bad) == 0, f"fast loop differs at {v[bad[:5]]}: {full[bad[:5]]} vs {ref[bad[:5]]}"
         bad = np.nonzero(lit != ref)[0]
         assert len(bad) == 0, f"literal loop differs at {v[bad[:5]]}"
+        assert not np.any(cert == 3), f"A={A}: branch-free certify_fast disagrees with dp_certify at {v[cert == 3][:5]}"
         ok = cert == 1
         assert np.all((ref[ok] >= 0) & (ref[ok] <= A)), f"A={A}: certified a value the oracle rejects"
         assert np.all(ref[cert == 2] == -1), f"A={A}: certified exception the oracle accepts"
