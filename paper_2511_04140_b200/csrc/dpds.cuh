@@ -156,8 +156,7 @@ __device__ __forceinline__ int certify_fast(double v, int A, double p, int64_t* 
     const bool special = ef == 0 || ef == 0x7ffu;
     const int e2 = (int)ef - 1023;
     const int k0 = (e2 * 78913) >> 18;
-    const int ki = k0 + 1 < 308 ? k0 + 1 : 308;
-    const int mag = k0 + ((b & ~X::SIGN) >= X::dec(ki) ? 1 : 0);
+    const int mag = k0 + ((b & ~X::SIGN) >= X::dec(k0 + 1) ? 1 : 0);  // table has a guard entry
     const bool inrange = A + mag >= 0 && A + mag <= X::MAXB - 1;
     // gap test: |s - rint(s)| <= ulp(s)  (valid for |s| >= 1/2, guaranteed when inrange)
     const double s = __dmul_rn(v, p);
@@ -191,8 +190,7 @@ __device__ __forceinline__ int certify_fast(float v, int A, float p, int32_t* g,
     const bool special = ef == 0 || ef == 0xffu;
     const int e2 = (int)ef - 127;
     const int k0 = (e2 * 78913) >> 18;
-    const int ki = k0 + 1 < 38 ? k0 + 1 : 38;
-    const int mag = k0 + (ab >= X::dec(ki) ? 1 : 0);
+    const int mag = k0 + (ab >= X::dec(k0 + 1) ? 1 : 0);  // table has a guard entry
     const bool inrange = A + mag >= 0 && A + mag <= X::MAXB - 1;
     const float s = __fmul_rn(v, p);
     const float r = rintf(s);

@@ -84,8 +84,8 @@ __device__ __forceinline__ uint32_t nonzero_bytes(uint32_t w) {
     return ((((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w) >> 7) & 0x01010101u;
 }
 
-template <typename T, int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1)
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT : 1))
     encode_chunks_kernel(const T* __restrict__ in, geometry g, uint8_t* __restrict__ out,
                          uint64_t out_cap, encode_ws ws) {
     using tr = lane_traits<T>;
@@ -99,28 +99,28 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1)
     const int NC = (int)((n - 1) / 8);  // row bytes = byte columns
     const int BM = NC / 8;              // sparse bitmap bytes
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nwarps = blockDim.x >> 5;
-    const int PT = (int)blockDim.x;
+    constexpr int nwarps = NT / 32;
+    constexpr int PT = NT;
 
     uint8_t* s_stage = smem;  // chunk image (phase 0)
     // [block][thread] u64: byte k of entry (s, t) = row byte t of bit plane 8s+k
     uint64_t* s_planes = reinterpret_cast<uint64_t*>(smem + encode_stage_bytes<T>(n));
 
-    __shared__ uint32_t s_flag1[32], s_flag2[32];  // per warp: bit 31 exception | one-hot alphas
-    __shared__ uint32_t s_mag[32];                 // per warp: max floor_log10 + 1024 (0: none)
-    __shared__ uint32_t s_warpw[32];
-    __shared__ uint32_t s_rowoff[64];
-    __shared__ uint32_t s_nzc[32][16];   // per warp: 8-bit nonzero-byte counters, 4 planes/word
-    __shared__ uint16_t s_wpre[64 * 32]; // nonzero bytes of plane p in warps before w
+    __shared__ uint32_t s_flag1[nwarps], s_flag2[nwarps];  // bit 31 exception | one-hot alphas
+    __shared__ uint32_t s_mag[nwarps];                     // max floor_log10 + 1024 (0: none)
+    __shared__ uint32_t s_warpw[nwarps];
+    __shared__ uint32_t s_rowinfo[64];       // plane p: dense << 31 | row offset in the image
+    __shared__ uint32_t s_nzc[nwarps][16];   // 8-bit nonzero-byte counters, 4 planes/word
+    __shared__ uint16_t s_wpre[64 * nwarps]; // nonzero bytes of plane p in warps before w
     __shared__ uint64_t s_dense;
     __shared__ uint32_t s_size;
     __shared__ B s_z1;
 
-    const uint64_t c = blockIdx.x;
-    const uint64_t b = g.batch_of(c);
-    const uint32_t ci = (uint32_t)(c - b * g.cpb);
+    const uint32_t c = blockIdx.x;                 // < 2^31 chunks per launch
+    const uint32_t b = c / g.cpb;
+    const uint32_t ci = c - b * g.cpb;
     const uint64_t bcount = g.values_in(b);
-    const uint64_t v0 = b * g.batch_values + (uint64_t)ci * n;
+    const uint64_t v0 = (uint64_t)b * g.batch_values + (uint64_t)ci * n;
     const uint64_t left = bcount - (uint64_t)ci * n;
     const uint32_t len = left < n ? (uint32_t)left : n;  // short final chunk: +0.0 padding
     const bool active = tid < NC;
@@ -129,33 +129,31 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1)
     T v[8];
     T vprev = T(0);
     {
-        const T* src = in + v0;
-        const uint32_t i0 = 8u * (uint32_t)tid;
+        const T* src = in + v0 + 8u * (uint32_t)tid;
+        if (len == n && NC == NT) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = (active && i0 + 1 + j < len) ? __ldg(src + i0 + 1 + j) : T(0);
-        if (active && i0 < len) vprev = __ldg(src + i0);
-    }
-    // the image is built on a zeroed buffer: zero bytes are never written
-    {
-        uint4* st = reinterpret_cast<uint4*>(s_stage);
-        const int words = (int)(encode_stage_bytes<T>(n) >> 4);
-        for (int i = tid; i < words; i += PT) st[i] = make_uint4(0u, 0u, 0u, 0u);
+            for (int j = 0; j < 8; ++j) v[j] = __ldg(src + 1 + j);
+            vprev = __ldg(src);
+        } else {
+            const uint32_t i0 = 8u * (uint32_t)tid;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = (active && i0 + 1 + j < len) ? __ldg(src + 1 + j) : T(0);
+            if (active && i0 < len) vprev = __ldg(src);
+        }
     }
 
     // ---- analyze, phase 1: exact loop on one sample per thread -> A0 ----
+    // (thread 0 samples value 0, which phase 2 does not see; value 1 is certified there)
     uint32_t f1 = 0;
     if (active) {
-        const int a = dp_alpha_full<T>(v[0]);
+        const int a = dp_alpha_full<T>(tid == 0 ? vprev : v[0]);
         f1 = a < 0 ? 0x80000000u : (1u << a);
-    }
-    if (tid == 0) {  // value 0 is analysed by thread 0 only
-        const int a = dp_alpha_full<T>(vprev);
-        f1 |= a < 0 ? 0x80000000u : (1u << a);
     }
     f1 = __reduce_or_sync(0xffffffffu, f1);
     if (lane == 0) s_flag1[warp] = f1;
     __syncthreads();
     uint32_t F = 0;
+#pragma unroll
     for (int i = 0; i < nwarps; ++i) F |= s_flag1[i];
     const int A0 = (F & 0x7fffffffu) ? 31 - __clz((int)(F & 0x7fffffffu)) : 0;
 
@@ -199,6 +197,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1)
     }
     __syncthreads();
     uint32_t M = 0;
+#pragma unroll
     for (int i = 0; i < nwarps; ++i) {
         F |= s_flag2[i];
         M = s_mag[i] > M ? s_mag[i] : M;
@@ -264,18 +263,20 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1)
     __syncthreads();
 
     int w = 0;
+#pragma unroll
     for (int i = 0; i < nwarps; ++i) w = (int)s_warpw[i] > w ? (int)s_warpw[i] : w;
     const int fb = (w + 7) >> 3;
 
     // ---- sizes and row offsets (warp 0): plane p is row w-1-p ----
     if (warp == 0) {
         uint32_t nz0 = 0, nz1 = 0;  // nonzero bytes of planes `lane` and `lane + 32`
+#pragma unroll
         for (int q = 0; q < nwarps; ++q) {
             const int wq = (int)s_warpw[q];
             const uint32_t c0 = lane < wq ? (s_nzc[q][lane >> 2] >> (8 * (lane & 3))) & 0xffu : 0u;
             const uint32_t c1 = lane + 32 < wq ? (s_nzc[q][(lane + 32) >> 2] >> (8 * (lane & 3))) & 0xffu : 0u;
-            s_wpre[lane * 32 + q] = (uint16_t)nz0;
-            s_wpre[(lane + 32) * 32 + q] = (uint16_t)nz1;
+            s_wpre[lane * nwarps + q] = (uint16_t)nz0;
+            s_wpre[(lane + 32) * nwarps + q] = (uint16_t)nz1;
             nz0 += c0;
             nz1 += c1;
         }
@@ -302,8 +303,8 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1)
         const uint32_t tot1 = __shfl_sync(0xffffffffu, s1, 0);
         const uint32_t tot0 = __shfl_sync(0xffffffffu, s0, 0);
         const uint32_t base = HDR + fb;
-        s_rowoff[lane + 32] = base + (s1 - c1);
-        s_rowoff[lane] = base + tot1 + (s0 - c0);
+        s_rowinfo[lane + 32] = (base + (s1 - c1)) | (d1 ? 0x80000000u : 0u);
+        s_rowinfo[lane] = (base + tot1 + (s0 - c0)) | (d0 ? 0x80000000u : 0u);
         const uint32_t dm0 = __ballot_sync(0xffffffffu, d0);
         const uint32_t dm1 = __ballot_sync(0xffffffffu, d1);
         const uint32_t size = w ? base + tot1 + tot0 : (uint32_t)HDR;
@@ -332,24 +333,37 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1)
     const int wblk = (w + 7) >> 3;
     for (int sb = 0; sb < wblk; ++sb) {
         const uint64_t y = sb < nblk ? s_planes[sb * PT + tid] : 0ull;  // above warp_w: zero
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        const int kmax = w - 8 * sb < 8 ? w - 8 * sb : 8;
+        if (kmax == 8 && ((dense >> (8 * sb)) & 0xffu) == 0xffu) {
+            // eight dense rows, consecutive in the image (plane 8sb+7 first): one base
+            // address, immediate offsets
+            uint8_t* r7 = s_stage + (s_rowinfo[8 * sb + 7] & 0x7fffffffu) + tid;
+            if (active) {
+                const uint32_t lo = (uint32_t)y, hi = (uint32_t)(y >> 32);
+                r7[0 * NC] = (uint8_t)(hi >> 24);
+                r7[1 * NC] = (uint8_t)(hi >> 16);
+                r7[2 * NC] = (uint8_t)(hi >> 8);
+                r7[3 * NC] = (uint8_t)hi;
+                r7[4 * NC] = (uint8_t)(lo >> 24);
+                r7[5 * NC] = (uint8_t)(lo >> 16);
+                r7[6 * NC] = (uint8_t)(lo >> 8);
+                r7[7 * NC] = (uint8_t)lo;
+            }
+            continue;
+        }
+        for (int k = 0; k < kmax; ++k) {
             const int p = 8 * sb + k;
-            if (p < w) {
-                const uint32_t byte = (uint32_t)(y >> (8 * k)) & 0xffu;
-                uint8_t* row = s_stage + s_rowoff[p];
-                if ((dense >> p) & 1) {
-                    if (byte) row[tid] = (uint8_t)byte;
-                } else {
-                    // bitmap: byte j nonzero -> bit 7-j%8 of bitmap byte j/8; then the
-                    // nonzero bytes in order (bitplane.hpp:126-148)
-                    const uint32_t m = __ballot_sync(0xffffffffu, byte != 0);
-                    if (m) {
-                        const uint32_t bm8 = __brev(m >> lane) >> 24;
-                        if ((lane & 7) == 0 && (bm8 & 0xffu)) row[tid >> 3] = (uint8_t)bm8;
-                        if (byte) row[BM + s_wpre[p * 32 + warp] + __popc(m & lt_mask)] = (uint8_t)byte;
-                    }
-                }
+            const uint32_t info = s_rowinfo[p];
+            uint8_t* row = s_stage + (info & 0x7fffffffu);
+            const uint32_t byte = (uint32_t)(y >> (8 * k)) & 0xffu;
+            if (info >> 31) {
+                if (active) row[tid] = (uint8_t)byte;
+            } else {
+                // bitmap: byte j nonzero -> bit 7-j%8 of bitmap byte j/8; then the nonzero
+                // bytes in order (bitplane.hpp:126-148)
+                const uint32_t m = __ballot_sync(0xffffffffu, byte != 0);
+                if ((lane & 7) == 0 && active) row[tid >> 3] = (uint8_t)(__brev(m >> lane) >> 24);
+                if (byte) row[BM + s_wpre[p * nwarps + warp] + __popc(m & lt_mask)] = (uint8_t)byte;
             }
         }
     }
@@ -512,9 +526,11 @@ __global__ void __launch_bounds__(kPlaceTile) place_chunks_kernel(geometry g, ui
     }
 }
 
+// one thread per byte column, rounded to an instantiated CTA size
 uint32_t encode_block_threads(uint32_t chunk_n) {
     const uint32_t nc = (chunk_n - 1) / 8;
-    return nc < 32 ? 32 : ((nc + 31) / 32) * 32;
+    if (nc <= 256) return nc < 32 ? 32 : ((nc + 31) / 32) * 32;
+    return nc <= 512 ? 512 : 1024;
 }
 
 template <typename T>
@@ -585,7 +601,21 @@ cudaError_t launch_encode(const T* d_in, const geometry& g, uint8_t* d_out, uint
     if ((e = cudaMemsetAsync(ws.ticket, 0, sizeof(uint32_t), st))) return e;
     const uint32_t threads = encode_block_threads(g.chunk_n);
     const uint32_t smem = encode_smem_bytes<T>(g.chunk_n);
-    auto kern = threads <= 256 ? encode_chunks_kernel<T, 256> : encode_chunks_kernel<T, 1024>;
+    void (*kern)(const T*, geometry, uint8_t*, uint64_t, encode_ws);
+    switch (threads) {
+    case 32: kern = encode_chunks_kernel<T, 32>; break;
+    case 64: kern = encode_chunks_kernel<T, 64>; break;
+    case 96: kern = encode_chunks_kernel<T, 96>; break;
+    case 128: kern = encode_chunks_kernel<T, 128>; break;
+    case 160: kern = encode_chunks_kernel<T, 160>; break;
+    case 192: kern = encode_chunks_kernel<T, 192>; break;
+    case 224: kern = encode_chunks_kernel<T, 224>; break;
+    case 256: kern = encode_chunks_kernel<T, 256>; break;
+    case 512: kern = encode_chunks_kernel<T, 512>; break;
+    case 1024: kern = encode_chunks_kernel<T, 1024>; break;
+    default: kern = nullptr;
+    }
+    if (!kern) return cudaErrorInvalidConfiguration;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
     if (ev0 && (e = cudaEventRecord(ev0, st))) return e;
     kern<<<(unsigned)g.n_chunks, threads, smem, st>>>(d_in, g, d_out, out_cap, ws);

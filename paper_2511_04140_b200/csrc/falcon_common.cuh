@@ -57,8 +57,8 @@ template <> struct lane_traits<float> {
 #ifdef FB200_KERNEL_TU
 __device__ double g_pow10_f64[23];
 __device__ float g_pow10_f32[11];
-__device__ uint64_t g_decade_f64[617];
-__device__ uint32_t g_decade_f32[77];
+__device__ uint64_t g_decade_f64[618];  // + guard entry (+inf) for exponent 0x7ff
+__device__ uint32_t g_decade_f32[78];   // + guard entry (+inf) for exponent 0xff
 #endif
 
 // Device error word: ((key) << 8) | code, lowest key wins (atomicMin).

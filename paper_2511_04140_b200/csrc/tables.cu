@@ -20,8 +20,10 @@ cudaError_t upload_tables() {
     for (int i = 0; i < 23; ++i, d *= 10.0) p64[i] = d;
     float f = 1.0f;
     for (int i = 0; i < 11; ++i, f *= 10.0f) p32[i] = f;
-    uint64_t dec64[617];
-    uint32_t dec32[77];
+    uint64_t dec64[618];
+    uint32_t dec32[78];
+    dec64[617] = 0x7ff0000000000000ull;  // guard: only read for inf/nan lanes
+    dec32[77] = 0x7f800000u;
     char buf[16];
     for (int k = -308; k <= 308; ++k) {
         std::snprintf(buf, sizeof buf, "1e%d", k);
