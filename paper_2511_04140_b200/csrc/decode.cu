@@ -14,6 +14,7 @@
 //   planes  thread t owns byte column t: 8x8 transposes rebuild lanes 8t..8t+7
 //   scan    block-wide wrapping inclusive scan of unzigzagged deltas (transform.hpp:91-106)
 //   values  Case 1: (T)g / 10^alpha (IEEE division), Case 2: raw bits; coalesced stores
+#include "dpds.cuh"
 #include "falcon_common.cuh"
 #include "kernels.h"
 
@@ -101,38 +102,60 @@ __device__ void walk_frames(const uint8_t* __restrict__ arc, uint64_t len, const
 
 }  // namespace
 
-template <typename T, int MAXT>
-__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1) decode_chunks_kernel(const uint8_t* __restrict__ arc,
-                                                             uint64_t len, geometry g,
-                                                             T* __restrict__ out, decode_ws ws) {
+// RN(g / p) for the Case-1 inverse scale (numeric.hpp:159-162): one Markstein
+// correction step from the rounded reciprocal, accepted only when the exact residual
+// test of dpds.cuh (2) proves it is the correctly rounded quotient; otherwise IEEE
+// division.  f32 keeps the IEEE division.
+__device__ __noinline__ double ddiv_fallback(double a, double b) { return __ddiv_rn(a, b); }
+
+__device__ __forceinline__ double inverse_scale_rn(double gd, double p, double rp) {
+    const double q0 = __dmul_rn(gd, rp);
+    const double r = __fma_rn(-q0, p, gd);
+    const double q = __fma_rn(r, rp, q0);
+    // q == RN(gd / p) iff |gd - q*p| < p * ulp(q) / 2 (halved below a power of two when
+    // the quotient lies below q); the residual is exact (dpds.cuh (2)).  Ties and
+    // anything not proven take the IEEE division.
+    const double e = __fma_rn(-q, p, gd);
+    const int qhi = __double2hiint(q);
+    const uint32_t qe = ((uint32_t)qhi >> 20) & 0x7ffu;
+    const bool pow2 = (qhi & 0x000fffff) == 0 && __double2loint(q) == 0;
+    const bool toward0 = (__double2hiint(e) ^ qhi) < 0;
+    const double H = __dmul_rn(p, __hiloint2double((int)((qe - 53u - ((pow2 && toward0) ? 1u : 0u)) << 20), 0));
+    if (fabs(e) < H && qe > 53u) return q;
+    return ddiv_fallback(gd, p);
+}
+__device__ __forceinline__ float inverse_scale_rn(float gf, float p, float) { return __fdiv_rn(gf, p); }
+
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT : 1))
+    decode_chunks_kernel(const uint8_t* __restrict__ arc, uint64_t len, geometry g,
+                         T* __restrict__ out, decode_ws ws) {
     using tr = lane_traits<T>;
     using B = typename tr::B;
     using S = typename tr::S;
     constexpr int W = tr::width;
     constexpr int HDR = tr::header;
+    constexpr int nwarps = NT / 32;
 
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t n = g.chunk_n;
     const int NC = (int)((n - 1) / 8);
     const int BM = NC / 8;  // sparse bitmap bytes (bitplane.hpp:113-122)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nwarps = blockDim.x >> 5;
+    const bool active = tid < NC;
 
     const uint32_t pn = pidx(n) + 1;
     uint32_t region = (uint32_t)(pn * sizeof(T) + 15) & ~15u;
     const uint32_t stage_need = (uint32_t)(HDR + (W + 7) / 8 + W * NC + 16 + 15) & ~15u;
     region = stage_need > region ? stage_need : region;
-    uint8_t* s_stage = smem;                       // chunk bytes, then output values
-    T* s_out = reinterpret_cast<T*>(smem);
-    uint8_t* s_rows = smem + region;               // [W][NC]
+    uint8_t* s_stage = smem;  // chunk bytes, then output values
 
     __shared__ uint32_t s_ticket, s_abort, s_code, s_w, s_hA;
     __shared__ uint64_t s_off;
     __shared__ uint32_t s_size;
-    __shared__ uint64_t s_dense;
     __shared__ B s_z1;
-    __shared__ uint32_t s_rowoff[64];
-    __shared__ B s_wtot[32];
+    __shared__ uint32_t s_rowinfo[64];        // plane p: dense << 31 | row offset in the chunk
+    __shared__ B s_wtot[nwarps];
 
     if (tid == 0) s_ticket = atomicAdd(ws.ticket, 1u);
     __syncthreads();
@@ -140,11 +163,11 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1) decode_ch
         walk_frames(arc, len, g, ws);
         return;
     }
-    const uint64_t c = s_ticket - 1;
-    const uint64_t b = g.batch_of(c);
-    const uint32_t ci = (uint32_t)(c - b * g.cpb);
+    const uint32_t c = s_ticket - 1;  // < 2^31 chunks per launch
+    const uint32_t b = c / g.cpb;
+    const uint32_t ci = c - b * g.cpb;
     const uint64_t bcount = g.values_in(b);
-    const uint64_t v0 = b * g.batch_values + (uint64_t)ci * n;
+    const uint64_t v0 = (uint64_t)b * g.batch_values + (uint64_t)ci * n;
     const uint64_t left = bcount - (uint64_t)ci * n;
     const uint32_t count = left < n ? (uint32_t)left : n;
 
@@ -175,8 +198,8 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1) decode_ch
     const bool src_aligned = ((uintptr_t)arc & 15) == 0;
     if (end <= region) {
         const uint32_t nvec = (end + 15) >> 4;
-        for (uint32_t v = tid; v < nvec; v += blockDim.x) {
-            const uint32_t lo = v << 4;
+        for (uint32_t vv = tid; vv < nvec; vv += NT) {
+            const uint32_t lo = vv << 4;
             if (src_aligned && (off - a) + lo + 16 <= len) {
                 *reinterpret_cast<uint4*>(s_stage + lo) = __ldg(reinterpret_cast<const uint4*>(src + lo));
             } else {
@@ -188,24 +211,19 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1) decode_ch
     __syncthreads();
 
     // ---- parse + validate in the reference's order (chunk_codec.hpp:92-117,
-    //      bitplane.hpp:160-186); warp 0 walks the rows, popcounts in parallel ----
+    //      bitplane.hpp:160-186); warp 0 walks the rows, popcounts + warp prefixes
+    //      of sparse bitmaps in parallel ----
     if (warp == 0) {
         const uint8_t* p = s_stage + a;
+        // a chunk longer than any valid one cannot be staged: read its header from global
+        const bool oversize = end > region;
+        const uint8_t* hp = oversize ? arc + off : p;
         uint32_t code = 0, w = 0, hA = 0;
         uint64_t flags = 0;
         B z1 = 0;
-        if (end > region || size < (uint32_t)HDR) {
+        if (size < (uint32_t)HDR) {
             code = DEV_E_HDR_TRUNC;
-            if (end > region) {
-                // longer than any valid chunk: the row walk must end in a size mismatch or
-                // truncation; decide it from the header alone is not possible, so report
-                // the first check that such a chunk fails below after reading the header
-                code = 0;
-            }
-        }
-        // an oversized chunk cannot be staged; read its header straight from global
-        const uint8_t* hp = end > region ? arc + off : p;
-        if (!code) {
+        } else {
             hA = hp[0];
             const uint32_t hB = hp[1];
             const bool case2 = hA > (uint32_t)tr::max_alpha || hB > (uint32_t)tr::max_beta;
@@ -227,35 +245,58 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1) decode_ch
                     pos += fb;
                 }
             }
-            if (!code && end > region) {
-                code = DEV_E_SIZE;  // no valid chunk of this geometry is that long
-            }
-            if (!code) {
-                for (int r = 0; r < (int)w; ++r) {
-                    const int pb = (int)w - 1 - r;
-                    if ((flags >> pb) & 1) {
-                        if (size - pos < (uint32_t)NC) { code = DEV_E_ROW_TRUNC; break; }
-                        if (lane == 0) s_rowoff[pb] = pos;
-                        pos += NC;
-                    } else {
-                        if (size - pos < (uint32_t)BM) { code = DEV_E_BITMAP_TRUNC; break; }
-                        if (lane == 0) s_rowoff[pb] = pos;
-                        uint32_t cntp = 0;
-                        for (int k = lane; k < BM; k += 32) cntp += __popc(p[pos + k]);
-                        cntp = __reduce_add_sync(0xffffffffu, cntp);
-                        pos += BM;
-                        if (size - pos < cntp) { code = DEV_E_PAYLOAD_TRUNC; break; }
-                        pos += cntp;
-                    }
+            if (!code && oversize) code = DEV_E_SIZE;  // no valid chunk of this geometry is that long
+            if (!code && w > 0) {
+                // Row walk (bitplane.hpp:160-186).  Row r (plane w-1-r) sits at
+                //   pos0 + NC * #dense rows before r + sum over sparse rows before r of (BM + popcount)
+                // Lane L owns rows L and L+32; only the sparse rows' popcounts are sequential.
+                const uint32_t pos0 = pos;
+                const int r0 = lane, r1 = lane + 32;
+                const bool v0r = r0 < (int)w, v1r = r1 < (int)w;
+                const bool d0 = v0r && ((flags >> (w - 1 - r0)) & 1);
+                const bool d1 = v1r && ((flags >> (w - 1 - r1)) & 1);
+                const uint32_t dm0 = __ballot_sync(0xffffffffu, d0), dm1 = __ballot_sync(0xffffffffu, d1);
+                const uint32_t sm0 = __ballot_sync(0xffffffffu, v0r && !d0), sm1 = __ballot_sync(0xffffffffu, v1r && !d1);
+                const uint32_t lt = (1u << lane) - 1u;
+                const uint32_t nd0 = __popc(dm0 & lt), nd1 = __popc(dm0) + __popc(dm1 & lt);
+                uint32_t acc0 = 0, acc1 = 0;  // sparse bytes before rows r0 / r1
+                uint32_t acc = 0;             // sparse bytes so far
+                int bad = 64;                 // first row failing a truncation check
+                uint32_t bad_code = 0;
+                uint64_t sparse = ((uint64_t)sm1 << 32) | sm0;
+                while (sparse) {
+                    const int r = __ffsll((long long)sparse) - 1;
+                    sparse &= sparse - 1;
+                    const uint32_t nd = r < 32 ? __popc(dm0 & ((1u << r) - 1u))
+                                               : __popc(dm0) + __popc(dm1 & ((1u << (r - 32)) - 1u));
+                    const uint32_t rp = pos0 + nd * (uint32_t)NC + acc;
+                    if (size < rp + (uint32_t)BM) { bad = r; bad_code = DEV_E_BITMAP_TRUNC; break; }
+                    uint32_t pc = 0;
+                    for (int k = lane; k < BM; k += 32) pc += __popc(p[rp + k]);
+                    pc = __reduce_add_sync(0xffffffffu, pc);
+                    if (size - rp - (uint32_t)BM < pc) { bad = r; bad_code = DEV_E_PAYLOAD_TRUNC; break; }
+                    if (r0 > r) acc0 += (uint32_t)BM + pc;
+                    if (r1 > r) acc1 += (uint32_t)BM + pc;
+                    acc += (uint32_t)BM + pc;
                 }
-                if (!code && pos != size) code = DEV_E_SIZE;
+                const uint32_t pr0 = pos0 + nd0 * (uint32_t)NC + acc0;
+                const uint32_t pr1 = pos0 + nd1 * (uint32_t)NC + acc1;
+                // dense rows truncated before the first sparse failure (reference order)
+                const uint32_t t0 = __ballot_sync(0xffffffffu, d0 && r0 < bad && size - pr0 < (uint32_t)NC);
+                const uint32_t t1 = __ballot_sync(0xffffffffu, d1 && r1 < bad && size - pr1 < (uint32_t)NC);
+                if (t0 | t1) code = DEV_E_ROW_TRUNC;
+                else if (bad_code) code = bad_code;
+                else if (pos0 + (uint32_t)(__popc(dm0) + __popc(dm1)) * (uint32_t)NC + acc != size) code = DEV_E_SIZE;
+                if (v0r) s_rowinfo[w - 1 - r0] = pr0 | (d0 ? 0x80000000u : 0u);
+                if (v1r) s_rowinfo[w - 1 - r1] = pr1 | (d1 ? 0x80000000u : 0u);
+            } else if (!code && pos != size) {
+                code = DEV_E_SIZE;
             }
         }
         if (lane == 0) {
             s_code = code;
             s_w = w;
             s_hA = hA;
-            s_dense = flags;
             s_z1 = z1;
         }
     }
@@ -265,48 +306,45 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1) decode_ch
         return;
     }
     const int w = (int)s_w;
-    const uint64_t dense = s_dense;
     const uint32_t hA = s_hA;
     const bool case2 = hA > (uint32_t)tr::max_alpha;
 
-    // ---- rows -> dense plane bytes, one warp per row ----
+    // ---- planes -> lanes: thread t gathers byte t of every row (dense: verbatim;
+    //      sparse: bitmap bit t, payload byte at warp prefix + ballot rank), then
+    //      8x8 transposes rebuild lanes 8t..8t+7 ----
+    const uint8_t* img = s_stage + a;
     const uint32_t lt_mask = (1u << lane) - 1u;
-    for (int p = warp; p < w; p += nwarps) {
-        const uint8_t* rs = s_stage + a + s_rowoff[p];
-        uint8_t* rd = s_rows + p * NC;
-        if ((dense >> p) & 1) {
-            for (int col = lane; col < NC; col += 32) rd[col] = rs[col];
-        } else {
-            const uint8_t* payload = rs + BM;
-            uint32_t running = 0;
-            for (int base = 0; base < NC; base += 32) {
-                const int col = base + lane;
-                const uint32_t bit = col < NC ? (rs[col >> 3] >> (7 - (col & 7))) & 1u : 0u;
-                const uint32_t m = __ballot_sync(0xffffffffu, bit);
-                if (col < NC) rd[col] = bit ? payload[running + __popc(m & lt_mask)] : (uint8_t)0;
-                running += __popc(m);
-            }
-        }
-    }
-    __syncthreads();
-
-    // ---- untranspose: byte column t -> lanes 8t..8t+7 ----
     B z[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) z[j] = 0;
-    if (tid < NC) {
-        const int nblk = (w + 7) >> 3;
-        for (int s = 0; s < nblk; ++s) {
-            uint64_t x = 0;
+    const int nblk = (w + 7) >> 3;
+    for (int sb = 0; sb < nblk; ++sb) {
+        uint32_t xb[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int p = 8 * s + k;
-                if (p < w) x |= (uint64_t)s_rows[p * NC + tid] << (8 * k);
+        for (int k = 0; k < 8; ++k) {
+            const int p = 8 * sb + k;
+            uint32_t byte = 0;
+            if (p < w) {
+                const uint32_t info = s_rowinfo[p];
+                const uint8_t* row = img + (info & 0x7fffffffu);
+                if (info >> 31) {
+                    if (active) byte = row[tid];
+                } else {
+                    // payload bytes of the warps before this one, then the ballot rank
+                    const uint32_t pre = __reduce_add_sync(0xffffffffu, lane < 4 * warp && lane < BM ? __popc(row[lane]) : 0u);
+                    const uint32_t bit = active ? (row[tid >> 3] >> (7 - (tid & 7))) & 1u : 0u;
+                    const uint32_t m = __ballot_sync(0xffffffffu, bit);
+                    if (bit) byte = row[BM + pre + __popc(m & lt_mask)];
+                }
             }
-            const uint64_t y = transpose8x8(x);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) z[j] |= (B)((y >> (8 * (7 - j))) & 0xffu) << (8 * s);
+            xb[k] = byte;
         }
+        const uint32_t xl = xb[0] | (xb[1] << 8) | (xb[2] << 16) | (xb[3] << 24);
+        const uint32_t xh = xb[4] | (xb[5] << 8) | (xb[6] << 16) | (xb[7] << 24);
+        const uint64_t y = transpose8x8(((uint64_t)xh << 32) | xl);
+        // byte 7-j of y is byte sb of lane j
+#pragma unroll
+        for (int j = 0; j < 8; ++j) z[j] |= (B)((y >> (8 * (7 - j))) & 0xffu) << (8 * sb);
     }
 
     // ---- inverse transform: wrapping inclusive scan (transform.hpp:97-100) ----
@@ -326,21 +364,25 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 1024 / MAXT : 1) decode_ch
     if (lane == 31) s_wtot[warp] = incl;
     __syncthreads();
     B before = s_z1;
-    for (int q = 0; q < warp; ++q) before += s_wtot[q];
+#pragma unroll
+    for (int q = 0; q < nwarps; ++q) before += q < warp ? s_wtot[q] : (B)0;
     before += incl - tsum;  // exclusive prefix of this thread
     const T scale = pow10_of(T{}, case2 ? 0 : (int)hA);
+    const T rscale = div_rn(T(1), scale);
     auto to_value = [&](B gv) -> T {
         if (case2) return value_of(unzigzag<B>(gv));
-        return div_rn(from_i64(T{}, (long long)(S)gv), scale);   // numeric.hpp:159-162
+        return inverse_scale_rn(from_i64(T{}, (long long)(S)gv), scale, rscale);  // numeric.hpp:159-162
     };
-    if (tid < NC) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) s_out[pidx(8 * tid + 1 + j)] = to_value((B)(before + d[j]));
-    }
-    if (tid == 0) s_out[pidx(0)] = to_value(s_z1);
-    __syncthreads();
+    // values straight from registers: thread t writes values 8t+1..8t+8 (a warp's eight
+    // stores cover 2 KB contiguously); padded lanes are dropped (transform.hpp:96)
     T* dst = out + v0;
-    for (uint32_t i = tid; i < count; i += blockDim.x) dst[i] = s_out[pidx(i)];
+    if (active) {
+        const uint32_t i0 = 8u * (uint32_t)tid + 1u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (i0 + j < count) dst[i0 + j] = to_value((B)(before + d[j]));
+    }
+    if (tid == 0 && count > 0) dst[0] = to_value(s_z1);
 }
 
 template <typename T>
@@ -351,7 +393,7 @@ uint32_t decode_smem_bytes(uint32_t chunk_n) {
     uint32_t region = (uint32_t)(pn * sizeof(T) + 15) & ~15u;
     const uint32_t stage = (uint32_t)(tr::header + (tr::width + 7) / 8 + tr::width * nc + 16 + 15) & ~15u;
     if (stage > region) region = stage;
-    return region + tr::width * nc;
+    return region;
 }
 
 template <typename T>
@@ -364,7 +406,21 @@ cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry
     if ((e = cudaMemsetAsync(ws.abort_at, 0xff, sizeof(unsigned long long), st))) return e;
     const uint32_t threads = encode_block_threads(g.chunk_n);
     const uint32_t smem = decode_smem_bytes<T>(g.chunk_n);
-    auto kern = threads <= 256 ? decode_chunks_kernel<T, 256> : decode_chunks_kernel<T, 1024>;
+    void (*kern)(const uint8_t*, uint64_t, geometry, T*, decode_ws);
+    switch (threads) {
+    case 32: kern = decode_chunks_kernel<T, 32>; break;
+    case 64: kern = decode_chunks_kernel<T, 64>; break;
+    case 96: kern = decode_chunks_kernel<T, 96>; break;
+    case 128: kern = decode_chunks_kernel<T, 128>; break;
+    case 160: kern = decode_chunks_kernel<T, 160>; break;
+    case 192: kern = decode_chunks_kernel<T, 192>; break;
+    case 224: kern = decode_chunks_kernel<T, 224>; break;
+    case 256: kern = decode_chunks_kernel<T, 256>; break;
+    case 512: kern = decode_chunks_kernel<T, 512>; break;
+    case 1024: kern = decode_chunks_kernel<T, 1024>; break;
+    default: kern = nullptr;
+    }
+    if (!kern) return cudaErrorInvalidConfiguration;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
     if (ev0 && (e = cudaEventRecord(ev0, st))) return e;
     kern<<<(unsigned)(g.n_chunks + 1), threads, smem, st>>>(d_archive, len, g, d_out, ws);
