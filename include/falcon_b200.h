@@ -49,7 +49,7 @@ typedef enum {
     FALCON_ERR_CUDA = 4,        /* CUDA runtime failure (message has the CUDA error) */
     FALCON_ERR_CALLBACK = 5,    /* a source/sink callback reported failure */
     FALCON_ERR_CAPACITY = 6,    /* caller-provided output buffer too small */
-    FALCON_ERR_UNSUPPORTED = 7  /* valid but not supported by this build (chunk_n > 8193) */
+    FALCON_ERR_UNSUPPORTED = 7  /* valid but not supported by this build (chunk_n > 4097) */
 } falcon_status;
 
 typedef enum { FALCON_F64 = 0, FALCON_F32 = 1 } falcon_precision;  /* container.hpp:15 tag */

@@ -119,9 +119,9 @@ falcon_status enqueue_decompress(falcon_ctx* ctx, int prec, const void* d_archiv
         return set_error(FALCON_ERR_INVALID, "archive precision does not match the requested value type");
     if (info->total_values > cap)
         return set_error(FALCON_ERR_CAPACITY, "value capacity too small for the archive");
-    if (info->chunk_n > 8193)
+    if (info->chunk_n > 4097)
         return set_error(FALCON_ERR_UNSUPPORTED,
-                         "chunk_n > 8193 is not supported by the sm_100a kernels of this build");
+                         "chunk_n > 4097 is not supported by the sm_100a kernels of this build");
     FB_TRY(make_geometry(info->total_values, info->chunk_n, info->batch_values ? info->batch_values : 1,
                          47, g));
     if (g.n_chunks == 0) {

@@ -126,10 +126,55 @@ __device__ __forceinline__ double inverse_scale_rn(double gd, double p, double r
 }
 __device__ __forceinline__ float inverse_scale_rn(float gf, float p, float) { return __fdiv_rn(gf, p); }
 
+// ---- mbarrier / cp.async helpers (producer -> consumer ring) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    }
+}
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+template <int NT>
+__device__ __forceinline__ void consumer_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+
+constexpr int kDecodeSlots = 3;
+enum : uint32_t { SLOT_CHUNK = 0, SLOT_SKIP = 1, SLOT_EXIT = 2 };
+struct slot_meta {
+    uint64_t off;
+    uint32_t chunk, size, kind;
+};
+
+template <typename T>
+__host__ __device__ __forceinline__ uint32_t decode_region_bytes(uint32_t chunk_n) {
+    using tr = lane_traits<T>;
+    const uint32_t nc = (chunk_n - 1) / 8;
+    return (uint32_t)(tr::header + (tr::width + 7) / 8 + tr::width * nc + 16 + 15) & ~15u;
+}
+
+// Persistent, warp-specialized decode.  Block 0 is the frame walker.  In every other
+// block the last warp is a producer: it takes chunk tickets, waits for the walker to
+// publish the chunk's batch, and streams the chunk bytes (16-B cp.async at the source's
+// 16-B phase) into a ring of kDecodeSlots smem slots; the other NT threads consume the
+// slots in order, so staging of chunk i+1, i+2 overlaps the decode of chunk i.
 template <typename T, int NT>
-__global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT : 1))
-    decode_chunks_kernel(const uint8_t* __restrict__ arc, uint64_t len, geometry g,
-                         T* __restrict__ out, decode_ws ws) {
+__global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* __restrict__ arc, uint64_t len,
+                                                                geometry g, T* __restrict__ out,
+                                                                decode_ws ws) {
     using tr = lane_traits<T>;
     using B = typename tr::B;
     using S = typename tr::S;
@@ -137,79 +182,112 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
     constexpr int HDR = tr::header;
     constexpr int nwarps = NT / 32;
 
+    if (blockIdx.x == 0) {
+        walk_frames(arc, len, g, ws);
+        return;
+    }
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t n = g.chunk_n;
     const int NC = (int)((n - 1) / 8);
     const int BM = NC / 8;  // sparse bitmap bytes (bitplane.hpp:113-122)
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool active = tid < NC;
+    const uint32_t region = decode_region_bytes<T>(n);
 
-    const uint32_t pn = pidx(n) + 1;
-    uint32_t region = (uint32_t)(pn * sizeof(T) + 15) & ~15u;
-    const uint32_t stage_need = (uint32_t)(HDR + (W + 7) / 8 + W * NC + 16 + 15) & ~15u;
-    region = stage_need > region ? stage_need : region;
-    uint8_t* s_stage = smem;  // chunk bytes, then output values
-
-    __shared__ uint32_t s_ticket, s_abort, s_code, s_w, s_hA;
-    __shared__ uint64_t s_off;
-    __shared__ uint32_t s_size;
+    __shared__ __align__(8) uint64_t s_full[kDecodeSlots], s_empty[kDecodeSlots];
+    __shared__ slot_meta s_meta[kDecodeSlots];
+    __shared__ uint32_t s_code, s_w, s_hA;
     __shared__ B s_z1;
-    __shared__ uint32_t s_rowinfo[64];        // plane p: dense << 31 | row offset in the chunk
+    __shared__ uint32_t s_rowinfo[64];  // plane p: dense << 31 | row offset in the chunk
     __shared__ B s_wtot[nwarps];
 
-    if (tid == 0) s_ticket = atomicAdd(ws.ticket, 1u);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kDecodeSlots; ++i) {
+            mbar_init(&s_full[i], 64);   // 32 copy-completion + 32 release arrivals
+            mbar_init(&s_empty[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
-    if (s_ticket == 0) {
-        walk_frames(arc, len, g, ws);
+
+    if ((int)threadIdx.x >= NT) {
+        // ===================== producer warp =====================
+        const int lane = threadIdx.x & 31;
+        const bool aligned = ((uintptr_t)arc & 15) == 0;
+        for (uint32_t it = 0;; ++it) {
+            const int sl = (int)(it % kDecodeSlots);
+            if (it >= (uint32_t)kDecodeSlots) mbar_wait(&s_empty[sl], ((it / kDecodeSlots) & 1) ^ 1);
+            uint32_t t = 0;
+            if (lane == 0) t = atomicAdd(ws.ticket, 1u);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            uint32_t kind = SLOT_CHUNK;
+            uint64_t off = 0;
+            uint32_t size = 0;
+            if (t >= g.n_chunks) {
+                kind = SLOT_EXIT;
+            } else if (lane == 0) {
+                const uint32_t b = t / g.cpb;
+                while (ld_acquire32(&ws.ready[b]) == 0) {
+                    if (*(volatile unsigned long long*)ws.abort_at <= b) {
+                        kind = SLOT_SKIP;
+                        break;
+                    }
+                    __nanosleep(64);
+                }
+                if (kind == SLOT_CHUNK) {
+                    off = ws.chunk_off[t];
+                    size = ws.chunk_size[t];
+                }
+            }
+            kind = __shfl_sync(0xffffffffu, kind, 0);
+            off = __shfl_sync(0xffffffffu, off, 0);
+            size = __shfl_sync(0xffffffffu, size, 0);
+            uint8_t* buf = smem + (size_t)sl * region;
+            if (kind == SLOT_CHUNK) {
+                const uint32_t a = (uint32_t)(off & 15);
+                const uint64_t base = off - a;
+                const uint32_t end = a + size;
+                if (end <= region) {
+                    const uint32_t nvec = (end + 15) >> 4;
+                    for (uint32_t vv = lane; vv < nvec; vv += 32) {
+                        const uint64_t gaddr = base + 16ull * vv;
+                        if (aligned && gaddr + 16 <= len) {
+                            cp_async16(buf + 16 * vv, arc + gaddr);
+                        } else {  // ragged archive end: plain byte copies
+                            for (uint32_t k = 0; k < 16; ++k)
+                                if (gaddr + k < len) buf[16 * vv + k] = arc[gaddr + k];
+                        }
+                    }
+                }
+            }
+            if (lane == 0) s_meta[sl] = slot_meta{off, t, size, kind};
+            cp_async_arrive(&s_full[sl]);
+            mbar_arrive(&s_full[sl]);
+            if (kind == SLOT_EXIT) break;
+        }
         return;
     }
-    const uint32_t c = s_ticket - 1;  // < 2^31 chunks per launch
-    const uint32_t b = c / g.cpb;
-    const uint32_t ci = c - b * g.cpb;
-    const uint64_t bcount = g.values_in(b);
-    const uint64_t v0 = (uint64_t)b * g.batch_values + (uint64_t)ci * n;
-    const uint64_t left = bcount - (uint64_t)ci * n;
-    const uint32_t count = left < n ? (uint32_t)left : n;
 
-    // ---- wait for the walker to publish this batch ----
-    if (tid == 0) {
-        s_abort = 0;
-        while (ld_acquire32(&ws.ready[b]) == 0) {
-            if (*(volatile unsigned long long*)ws.abort_at <= b) {
-                s_abort = 1;
-                break;
-            }
-            __nanosleep(128);
-        }
-        if (!s_abort) {
-            s_off = ws.chunk_off[c];
-            s_size = ws.chunk_size[c];
-        }
-    }
-    __syncthreads();
-    if (s_abort) return;
-    const uint64_t off = s_off;
-    const uint32_t size = s_size;
-
-    // ---- stage the chunk bytes at the source's 16-B phase ----
-    const uint32_t a = (uint32_t)(off & 15);
-    const uint8_t* src = arc + (off - a);
-    const uint32_t end = a + size;
-    const bool src_aligned = ((uintptr_t)arc & 15) == 0;
-    if (end <= region) {
-        const uint32_t nvec = (end + 15) >> 4;
-        for (uint32_t vv = tid; vv < nvec; vv += NT) {
-            const uint32_t lo = vv << 4;
-            if (src_aligned && (off - a) + lo + 16 <= len) {
-                *reinterpret_cast<uint4*>(s_stage + lo) = __ldg(reinterpret_cast<const uint4*>(src + lo));
-            } else {
-                const uint32_t from = lo > a ? lo : a, to = lo + 16 < end ? lo + 16 : end;
-                for (uint32_t i = from; i < to; ++i) s_stage[i] = src[i];
-            }
-        }
-    }
-    __syncthreads();
-
+    // ===================== consumer warps =====================
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool active = tid < NC;
+    for (uint32_t it = 0;; ++it) {
+        const int sl = (int)(it % kDecodeSlots);
+        mbar_wait(&s_full[sl], (it / kDecodeSlots) & 1);
+        const slot_meta meta = s_meta[sl];
+        if (meta.kind == SLOT_EXIT) break;
+        if (meta.kind == SLOT_CHUNK) {
+            const uint32_t c = meta.chunk;
+            const uint32_t b = c / g.cpb;
+            const uint32_t ci = c - b * g.cpb;
+            const uint64_t bcount = g.values_in(b);
+            const uint64_t v0 = (uint64_t)b * g.batch_values + (uint64_t)ci * n;
+            const uint64_t left = bcount - (uint64_t)ci * n;
+            const uint32_t count = left < n ? (uint32_t)left : n;
+            const uint64_t off = meta.off;
+            const uint32_t size = meta.size;
+            const uint32_t a = (uint32_t)(off & 15);
+            const uint32_t end = a + size;
+            uint8_t* s_stage = smem + (size_t)sl * region;
+            do {
     // ---- parse + validate in the reference's order (chunk_codec.hpp:92-117,
     //      bitplane.hpp:160-186); warp 0 walks the rows, popcounts + warp prefixes
     //      of sparse bitmaps in parallel ----
@@ -300,10 +378,10 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
             s_z1 = z1;
         }
     }
-    __syncthreads();
+    consumer_sync<NT>();
     if (s_code) {
         if (tid == 0) record_error(ws.error, c, s_code);
-        return;
+        break;
     }
     const int w = (int)s_w;
     const uint32_t hA = s_hA;
@@ -331,7 +409,9 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
                     if (active) byte = row[tid];
                 } else {
                     // payload bytes of the warps before this one, then the ballot rank
-                    const uint32_t pre = __reduce_add_sync(0xffffffffu, lane < 4 * warp && lane < BM ? __popc(row[lane]) : 0u);
+                    uint32_t pc = 0;
+                    for (int k = lane; k < 4 * warp && k < BM; k += 32) pc += __popc(row[k]);
+                    const uint32_t pre = __reduce_add_sync(0xffffffffu, pc);
                     const uint32_t bit = active ? (row[tid >> 3] >> (7 - (tid & 7))) & 1u : 0u;
                     const uint32_t m = __ballot_sync(0xffffffffu, bit);
                     if (bit) byte = row[BM + pre + __popc(m & lt_mask)];
@@ -362,7 +442,7 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
         if (lane >= k) incl += t;
     }
     if (lane == 31) s_wtot[warp] = incl;
-    __syncthreads();
+    consumer_sync<NT>();
     B before = s_z1;
 #pragma unroll
     for (int q = 0; q < nwarps; ++q) before += q < warp ? s_wtot[q] : (B)0;
@@ -383,17 +463,17 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
             if (i0 + j < count) dst[i0 + j] = to_value((B)(before + d[j]));
     }
     if (tid == 0 && count > 0) dst[0] = to_value(s_z1);
+
+            } while (0);
+        }
+        consumer_sync<NT>();
+        if (tid == 0) mbar_arrive(&s_empty[sl]);
+    }
 }
 
 template <typename T>
 uint32_t decode_smem_bytes(uint32_t chunk_n) {
-    using tr = lane_traits<T>;
-    const uint32_t nc = (chunk_n - 1) / 8;
-    const uint32_t pn = chunk_n + (chunk_n >> 3) + 1;
-    uint32_t region = (uint32_t)(pn * sizeof(T) + 15) & ~15u;
-    const uint32_t stage = (uint32_t)(tr::header + (tr::width + 7) / 8 + tr::width * nc + 16 + 15) & ~15u;
-    if (stage > region) region = stage;
-    return region;
+    return kDecodeSlots * decode_region_bytes<T>(chunk_n);
 }
 
 template <typename T>
@@ -422,8 +502,17 @@ cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry
     }
     if (!kern) return cudaErrorInvalidConfiguration;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    // persistent grid: every block co-resident (block 0 walks frames, the rest spin on it)
+    int per_sm = 0, dev = 0, sms = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)threads + 32, smem))) return e;
+    if ((e = cudaGetDevice(&dev))) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev))) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    uint64_t grid = (uint64_t)per_sm * sms;
+    if (grid > g.n_chunks + 1) grid = g.n_chunks + 1;
+    if (grid < 2) grid = 2;
     if (ev0 && (e = cudaEventRecord(ev0, st))) return e;
-    kern<<<(unsigned)(g.n_chunks + 1), threads, smem, st>>>(d_archive, len, g, d_out, ws);
+    kern<<<(unsigned)grid, threads + 32, smem, st>>>(d_archive, len, g, d_out, ws);
     if ((e = cudaGetLastError())) return e;
     return ev1 ? cudaEventRecord(ev1, st) : cudaSuccess;
 }

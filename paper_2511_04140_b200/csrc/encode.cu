@@ -79,6 +79,12 @@ __host__ __device__ __forceinline__ uint32_t encode_stage_bytes(uint32_t chunk_n
 __device__ __forceinline__ uint32_t lane_word(uint64_t z, int sb) { return sb < 4 ? (uint32_t)z : (uint32_t)(z >> 32); }
 __device__ __forceinline__ uint32_t lane_word(uint32_t z, int) { return z; }
 
+// st.shared.u8 under a predicate: no branch, no reconvergence block
+__device__ __forceinline__ void st_u8_if(bool p, uint8_t* addr, uint32_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.u8 [%1], %2;\n\t}"
+                 ::"r"((uint32_t)p), "r"((uint32_t)__cvta_generic_to_shared(addr)), "r"(v) : "memory");
+}
+
 // 0x01 in every nonzero byte of w
 __device__ __forceinline__ uint32_t nonzero_bytes(uint32_t w) {
     return ((((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w) >> 7) & 0x01010101u;
@@ -140,6 +146,16 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
             for (int j = 0; j < 8; ++j) v[j] = (active && i0 + 1 + j < len) ? __ldg(src + 1 + j) : T(0);
             if (active && i0 < len) vprev = __ldg(src);
         }
+    }
+
+    // zero the image buffer while the loads are in flight: bitmap and payload bytes of
+    // all-zero warp rows then need no store at all
+    {
+        uint4* st = reinterpret_cast<uint4*>(s_stage);
+        constexpr int kWords = 0;  // (runtime size below)
+        (void)kWords;
+        const int words = (int)(encode_stage_bytes<T>(n) >> 4);
+        for (int i = tid; i < words; i += PT) st[i] = make_uint4(0u, 0u, 0u, 0u);
     }
 
     // ---- analyze, phase 1: exact loop on one sample per thread -> A0 ----
@@ -351,19 +367,25 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
             }
             continue;
         }
-        for (int k = 0; k < kmax; ++k) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (k >= kmax) break;
             const int p = 8 * sb + k;
             const uint32_t info = s_rowinfo[p];
             uint8_t* row = s_stage + (info & 0x7fffffffu);
             const uint32_t byte = (uint32_t)(y >> (8 * k)) & 0xffu;
             if (info >> 31) {
-                if (active) row[tid] = (uint8_t)byte;
+                st_u8_if(active, row + tid, byte);
             } else {
                 // bitmap: byte j nonzero -> bit 7-j%8 of bitmap byte j/8; then the nonzero
-                // bytes in order (bitplane.hpp:126-148)
+                // bytes in order (bitplane.hpp:126-148).  The buffer is zeroed: a warp whose
+                // 32 bytes are all zero writes nothing.
                 const uint32_t m = __ballot_sync(0xffffffffu, byte != 0);
-                if ((lane & 7) == 0 && active) row[tid >> 3] = (uint8_t)(__brev(m >> lane) >> 24);
-                if (byte) row[BM + s_wpre[p * nwarps + warp] + __popc(m & lt_mask)] = (uint8_t)byte;
+                if (m) {
+                    const uint32_t bm8 = __brev(m >> lane) >> 24;
+                    st_u8_if((lane & 7) == 0 && bm8 != 0, row + (tid >> 3), bm8);
+                    st_u8_if(byte != 0, row + BM + s_wpre[p * nwarps + warp] + __popc(m & lt_mask), byte);
+                }
             }
         }
     }

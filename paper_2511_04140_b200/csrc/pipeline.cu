@@ -332,8 +332,8 @@ falcon_status run_decompress(falcon_ctx* ctx, int prec, const uint8_t* arc, uint
     if (h.precision != prec)
         return set_error(FALCON_ERR_INVALID, "archive precision does not match the requested value type");
     if (opt.n_streams == 0) return set_error(FALCON_ERR_INVALID, "stream count must be positive");
-    if (h.chunk_n > 8193)
-        return set_error(FALCON_ERR_UNSUPPORTED, "chunk_n > 8193 is not supported by the sm_100a kernels of this build");
+    if (h.chunk_n > 4097)
+        return set_error(FALCON_ERR_UNSUPPORTED, "chunk_n > 4097 is not supported by the sm_100a kernels of this build");
     if (io.dst && h.total_values > io.dst_cap)
         return set_error(FALCON_ERR_CAPACITY, "value capacity too small for the archive");
     const size_t esz = lane_bytes(prec);

@@ -63,9 +63,9 @@ falcon_status validate_options(uint32_t chunk_n, uint64_t batch_values) {
     if (chunk_n < 65 || (chunk_n - 1) % 64 != 0)
         return set_error(FALCON_ERR_INVALID, "chunk length must be a multiple of 64 plus one");
     if (batch_values == 0) return set_error(FALCON_ERR_INVALID, "batch size must be positive");
-    if (chunk_n > 8193)
+    if (chunk_n > 4097)
         return set_error(FALCON_ERR_UNSUPPORTED,
-                         "chunk_n > 8193 is not supported by the sm_100a kernels of this build");
+                         "chunk_n > 4097 is not supported by the sm_100a kernels of this build");
     return FALCON_OK;
 }
 

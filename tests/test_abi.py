@@ -28,7 +28,7 @@ def test_abi_version():
     assert fb.load().falcon_abi_version() == 1
 
 
-@pytest.mark.parametrize("prec,n", [(0, 65), (0, 1025), (1, 1025), (0, 8193)])
+@pytest.mark.parametrize("prec,n", [(0, 65), (0, 1025), (1, 1025), (0, 4097)])
 def test_max_encoded_chunk_size(oracle, prec, n):
     assert fb.max_encoded_chunk_size(prec, n) == oracle.max_chunk(prec, n)
 

@@ -64,7 +64,7 @@ def test_specials_take_raw_path(codec, oracle):
 @pytest.mark.parametrize("prec", [F64, F32])
 @pytest.mark.parametrize("kind", KINDS)
 @pytest.mark.parametrize("n,bv,count", [(65, 1000, 5000), (257, 257 * 3, 4000), (1025, 1025 * 4, 30000),
-                                         (1025, 1025 * 4096, 9000), (2049, 5000, 12000)])
+                                         (1025, 1025 * 4096, 9000), (2049, 5000, 12000), (4097, 9000, 20000)])
 def test_archive_parity_and_round_trip(codec, oracle, prec, kind, n, bv, count):
     vals = synth(kind, count, prec, dp=2 if prec == F64 else 1, seed=7 + count, period=100, block=n)
     want = oracle.compress_archive(vals, n, bv)
@@ -226,3 +226,8 @@ def test_large_outlier_round_trip_and_ratio(codec, oracle):
     want = oracle.compress_archive(sub, 1025, 4198400)
     a2, n2 = codec.compress_device(dev(sub))
     assert a2[:n2].cpu().numpy().tobytes() == want
+
+
+def test_unsupported_chunk_n_fails_loudly(codec):
+    with pytest.raises(FalconError, match="not supported"):
+        codec.compress_device(dev(np.zeros(9000)), chunk_n=8193, batch_values=9000)
