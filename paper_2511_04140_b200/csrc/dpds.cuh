@@ -214,6 +214,83 @@ __device__ __forceinline__ int certify_fast(float v, int A, float p, int32_t* g,
 }
 
 
+// ---- lean certification (the encoder's hot loop) ----
+// One-sided form of dp_certify: true only where dp_certify returns CERT_OK, with the
+// same lane integer; false means "undecided" (the exact loop decides).  Dropped
+// relative to dp_certify, each moving a rare case to the exact loop:
+//   * the gap test: with N = rint(s), |N - v*p| < p*ulp(v)/2 already implies
+//     |s - N| < ulp(s)/2 + p*2^(ev-53) < 1.5 ulp(s), and s - N is a multiple of ulp(s)
+//     (or zero), so the reference gap test (1) holds;
+//   * the per-value floor_log10: the range alpha0 <= A, A + mag <= max_beta - 1 is
+//     |v| >= dec(-A) and |v| < dec(max_beta - A); f64 compares high words strictly
+//     (equal high words -> undecided), f32 compares exactly;
+//   * powers of two (halved rounding interval) and exact ties (|e| == H).
+// The chunk-uniform parameters come from cert_params_for().
+template <typename T> struct cert_params;
+template <> struct cert_params<double> {
+    double p;         // 10^A
+    uint32_t lo1;     // hi(dec(-A)) + 1
+    uint32_t span;    // hi(dec(15 - A)) - hi(dec(-A)) - 1
+    uint32_t hk;      // hi(p) - (1076 << 20): hi word of H = p * 2^(ev - 53) is (ahi & EXP) + hk
+    uint32_t plo;     // lo(p)
+};
+template <> struct cert_params<float> {
+    float p;
+    double pd;        // (double)p
+    uint32_t lo;      // bits(dec(-A))
+    uint32_t span;    // bits(dec(6 - A)) - bits(dec(-A))
+    uint32_t hk;      // hi(pd) - (151 << 20): hi word of H = p * 2^(ev - 24) is ((ab & EXP) >> 3) + hk
+};
+
+__device__ __forceinline__ cert_params<double> cert_params_for(double, int A) {
+    using X = fpx<double>;
+    cert_params<double> c;
+    c.p = X::pow10(A);
+    const uint32_t L = (uint32_t)(X::dec(-A) >> 32), U = (uint32_t)(X::dec(X::MAXB - A) >> 32);
+    c.lo1 = L + 1u;
+    c.span = U > L + 1u ? U - L - 1u : 0u;
+    c.hk = (uint32_t)__double2hiint(c.p) - (1076u << 20);
+    c.plo = (uint32_t)__double2loint(c.p);
+    return c;
+}
+__device__ __forceinline__ cert_params<float> cert_params_for(float, int A) {
+    using X = fpx<float>;
+    cert_params<float> c;
+    c.p = X::pow10(A);
+    c.pd = (double)c.p;
+    c.lo = X::dec(-A);
+    c.span = X::dec(X::MAXB - A) - c.lo;
+    c.hk = (uint32_t)__double2hiint(c.pd) - (151u << 20);
+    return c;
+}
+
+// *g = rint(v * 10^A) (valid when true); *ah = |v|'s high word (f64) / bits (f32)
+__device__ __forceinline__ bool certify_lean(double v, const cert_params<double>& c, int64_t* g, uint32_t* ah) {
+    const uint32_t hi = (uint32_t)__double2hiint(v), lo = (uint32_t)__double2loint(v);
+    const uint32_t ahi = hi & 0x7fffffffu;
+    *ah = ahi;
+    const bool inr = (ahi - c.lo1) < c.span;
+    const bool notpow2 = ((ahi & 0x000fffffu) | lo) != 0u;
+    const double s = __dmul_rn(v, c.p);
+    const double r = rint(s);
+    const double e = __fma_rn(-v, c.p, r);  // exact (dpds (2))
+    const double H = __hiloint2double((int)((ahi & 0x7ff00000u) + c.hk), (int)c.plo);
+    *g = __double2ll_rz(r);
+    return inr && notpow2 && fabs(e) < H;
+}
+__device__ __forceinline__ bool certify_lean(float v, const cert_params<float>& c, int32_t* g, uint32_t* ah) {
+    const uint32_t ab = __float_as_uint(v) & 0x7fffffffu;
+    *ah = ab;
+    const bool inr = (ab - c.lo) < c.span;
+    const bool notpow2 = (ab & 0x007fffffu) != 0u;
+    const float s = __fmul_rn(v, c.p);
+    const float r = rintf(s);
+    const double e = __fma_rn(-(double)v, c.pd, (double)r);  // exact in double
+    const double H = __hiloint2double((int)(((ab & 0x7f800000u) >> 3) + c.hk), 0);
+    *g = (int32_t)__float2int_rz(r);
+    return inr && notpow2 && fabs(e) < H;
+}
+
 // (3): decide v against candidate scale A (0 <= A <= max_alpha).  CERT_OK: alpha_v <= A
 // and v is not an exception, *g = round_half_away(v*10^A).  CERT_EXC: v is an
 // exception.  CERT_UNDECIDED: run dp_alpha_full.

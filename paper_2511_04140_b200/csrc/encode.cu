@@ -158,58 +158,57 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
         for (int i = tid; i < words; i += PT) st[i] = make_uint4(0u, 0u, 0u, 0u);
     }
 
-    // ---- analyze, phase 1: exact loop on one sample per thread -> A0 ----
-    // (thread 0 samples value 0, which phase 2 does not see; value 1 is certified there)
-    uint32_t f1 = 0;
-    if (active) {
-        const int a = dp_alpha_full<T>(tid == 0 ? vprev : v[0]);
-        f1 = a < 0 ? 0x80000000u : (1u << a);
+    // ---- analyze, phase 1: warp 0 runs the exact loop on 32 samples spread over the
+    //      chunk -> A0 = the largest sampled alpha (attained, so alpha_max >= A0) ----
+    if (warp == 0) {
+        const uint32_t si = (uint32_t)lane * (n >> 5) + (n >> 6);
+        const T sv = si < len ? __ldg(in + v0 + si) : T(0);
+        const int a = dp_alpha_full<T>(sv);
+        const uint32_t f1 = __reduce_or_sync(0xffffffffu, a < 0 ? 0x80000000u : (1u << a));
+        if (lane == 0) s_flag1[0] = f1;
     }
-    f1 = __reduce_or_sync(0xffffffffu, f1);
-    if (lane == 0) s_flag1[warp] = f1;
     __syncthreads();
-    uint32_t F = 0;
-#pragma unroll
-    for (int i = 0; i < nwarps; ++i) F |= s_flag1[i];
+    uint32_t F = s_flag1[0];
     const int A0 = (F & 0x7fffffffu) ? 31 - __clz((int)(F & 0x7fffffffu)) : 0;
 
-    // ---- analyze, phase 2: certify every value against A0 (dpds.cuh (3)) ----
-    const T pA0 = X::pow10(A0);
+    // ---- analyze, phase 2: lean certification of every value at A0 (dpds.cuh); the
+    //      undecided ones (zeros, powers of two, decade edges, exceptions, alpha > A0)
+    //      run the exact loop.  Thread 0 also covers value 0 (bit 8). ----
     S gc[8];
-    uint32_t redo = 0;   // lanes whose lane integer must be recomputed at alpha_max
+    uint32_t redo = 0;   // values the exact loop decides
     uint32_t f2 = 0;     // exception bit | one-hot alphas of values decided by the exact loop
-    int magmax = INT_MIN;
+    uint32_t mx = 0;     // max |v| high word (f32: bits) -> floor_log10(max|v|) for beta_hat
     if (active && !(F >> 31)) {
+        const cert_params<T> cp = cert_params_for(T{}, A0);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            int mg;
-            const int r = certify_fast(v[j], A0, pA0, &gc[j], &mg);
-            magmax = mg > magmax ? mg : magmax;
-            f2 |= r == CERT_EXC ? 0x80000000u : 0u;
-            redo |= r == CERT_UNDECIDED ? (1u << j) : 0u;
+            uint32_t ah;
+            const bool ok = certify_lean(v[j], cp, &gc[j], &ah);
+            mx = ah > mx ? ah : mx;
+            redo |= ok ? 0u : (1u << j);
+        }
+        if (tid == 0) {
+            S g0;
+            uint32_t ah;
+            const bool ok = certify_lean(vprev, cp, &g0, &ah);
+            mx = ah > mx ? ah : mx;
+            redo |= ok ? 0u : 0x100u;
         }
         for (uint32_t rest = redo; rest; rest &= rest - 1) {  // rare: exact loop
             const int j = __ffs(rest) - 1;
-            T vj = v[0];
+            T vj = vprev;
 #pragma unroll
-            for (int q = 1; q < 8; ++q) vj = j == q ? v[q] : vj;
+            for (int q = 0; q < 8; ++q) vj = j == q ? v[q] : vj;
             const int a = dp_alpha_full<T>(vj);
             f2 |= a < 0 ? 0x80000000u : (1u << a);
-        }
-        if (tid == 0) {  // floor_log10 of value 0 for beta_hat
-            const B mb = X::bits(vprev) & ~X::SIGN;
-            const B ef = mb & X::EXPF;
-            if (mb != 0 && ef != 0 && ef != X::EXPF) {
-                const int mg = mag_of<T>(mb);
-                magmax = mg > magmax ? mg : magmax;
-            }
+            if (a < 0) break;  // the chunk is Case 2: nothing else matters
         }
     }
     f2 = __reduce_or_sync(0xffffffffu, f2);
-    const uint32_t mgw = __reduce_max_sync(0xffffffffu, magmax == INT_MIN ? 0u : (uint32_t)(magmax + 1024));
+    const uint32_t mxw = __reduce_max_sync(0xffffffffu, mx);
     if (lane == 0) {
         s_flag2[warp] = f2;
-        s_mag[warp] = mgw;
+        s_mag[warp] = mxw;
     }
     __syncthreads();
     uint32_t M = 0;
@@ -221,10 +220,40 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
     const int amax = (F & 0x7fffffffu) ? 31 - __clz((int)(F & 0x7fffffffu)) : 0;
     bool case2 = (F >> 31) != 0;
     int bhat = 0;
-    if (!case2) {  // transform.hpp:62-65; floor_log10(max|v|) = max floor_log10(|v|)
-        bhat = M == 0 ? 0 : amax + ((int)M - 1024) + 1;
-        case2 = amax > tr::max_alpha || bhat > tr::max_beta;
+    if (!case2 && M != 0) {  // transform.hpp:62-65: beta_hat = alpha_max + floor_log10(max|v|) + 1
+        int mag;
+        if constexpr (sizeof(T) == 4) {
+            mag = floor_log10_bits((uint32_t)M);
+        } else {
+            // only the high word of max|v| is known: exact unless a decade boundary
+            // falls inside it, then a second (uniform, rare) pass finds the low word
+            const int k0 = floor_log10_bits((uint64_t)M << 32);
+            const int k1 = floor_log10_bits((uint64_t)(((uint64_t)M << 32) | 0xffffffffu));
+            if (k0 == k1) {
+                mag = k0;
+            } else {
+                uint32_t ml = 0;
+                if (active) {
+#pragma unroll
+                    for (int j = 0; j < 9; ++j) {
+                        if (j == 8 && tid != 0) break;
+                        const uint64_t ab = (uint64_t)X::bits(j == 8 ? vprev : v[j < 8 ? j : 0]) & ~(uint64_t)X::SIGN;
+                        if ((uint32_t)(ab >> 32) == M && (uint32_t)ab > ml) ml = (uint32_t)ab;
+                    }
+                }
+                ml = __reduce_max_sync(0xffffffffu, ml);
+                __syncthreads();
+                if (lane == 0) s_mag[warp] = ml;
+                __syncthreads();
+                ml = 0;
+#pragma unroll
+                for (int i = 0; i < nwarps; ++i) ml = s_mag[i] > ml ? s_mag[i] : ml;
+                mag = floor_log10_bits(((uint64_t)M << 32) | ml);
+            }
+        }
+        bhat = amax + mag + 1;
     }
+    if (!case2) case2 = amax > tr::max_alpha || bhat > tr::max_beta;
     const uint32_t hA = case2 ? tr::exc_alpha : (uint32_t)amax;
     const uint32_t hB = case2 ? tr::exc_beta : (uint32_t)bhat;
 
@@ -240,15 +269,36 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
     B z[8];
     B orv = 0;
     {
+        // Case 1 at alpha_max == A0: every value has alpha_v <= A0, so v * 10^A0 lies within
+        // 3.5 ulp (<= 1/8) of its integer and rint == llround -- the certification's lane
+        // integers are final, also for the values the exact loop decided
         const bool reuse = !case2 && amax == A0;
-        B gp = lane_g(vprev);
-        if (tid == 0) s_z1 = gp;
+        const B gprev = lane_g(vprev);
+        if (tid == 0) s_z1 = gprev;
+        // f64 lanes whose integers all fit in 30 bits (|v| < 2^(28 - e_p), e_p = exponent
+        // of the scale) take 32-bit delta/zigzag arithmetic: same z, half the ALU work
+        const uint32_t lim = (2074u - ((uint32_t)__double2hiint((double)scale) >> 20)) << 20;
+        const bool narrow = sizeof(B) == 8 && __all_sync(0xffffffffu, reuse && mx < lim);
+        if (narrow) {
+            uint32_t gp = (uint32_t)gprev;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const B gj = (reuse && !((redo >> j) & 1)) ? (B)gc[j] : lane_g(v[j]);
-            z[j] = active ? zigzag<B>((B)(gj - gp)) : (B)0;
-            gp = gj;
-            orv |= z[j];
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t gj = (uint32_t)gc[j];
+                const uint32_t d = gj - gp;
+                const uint32_t zz = (d << 1) ^ (uint32_t)((int32_t)d >> 31);
+                z[j] = active ? (B)zz : (B)0;
+                gp = gj;
+                orv |= z[j];
+            }
+        } else {
+            B gp = gprev;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const B gj = reuse ? (B)gc[j] : lane_g(v[j]);
+                z[j] = active ? zigzag<B>((B)(gj - gp)) : (B)0;
+                gp = gj;
+                orv |= z[j];
+            }
         }
     }
     if (range_err) record_error(ws.error, c, DEV_E_SCALE);

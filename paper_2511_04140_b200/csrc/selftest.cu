@@ -4,8 +4,10 @@
 //   out_lit[i]  = literal reference loop         (dp_alpha: round(), IEEE division)
 //   out_cert[i] = dp_certify(v[i], A) code      (0 undecided, 1 ok, 2 exception)
 //   out_g[i]    = lane integer from certification (valid when code == 1)
-// and the branch-free encoder form certify_fast() must agree with dp_certify (code
-// 3 is written when they disagree, which the test treats as a failure).
+// with bit 2 set when the encoder's one-sided certify_lean() accepts the value.  The
+// branch-free certify_fast() must agree with dp_certify and certify_lean may only
+// accept what dp_certify certifies, with the same integer (-1 is written otherwise,
+// which the test treats as a failure).
 #include "dpds.cuh"
 #include "kernels.h"
 
@@ -25,7 +27,12 @@ __global__ void selftest_dp_kernel(const T* __restrict__ v, uint64_t n, int A, i
         typename fpx<T>::S gf = 0;
         int mg = 0;
         const int c2 = certify_fast(x, A, p, &gf, &mg);
-        out_cert[i] = (int8_t)((c1 == c2 && (c1 != CERT_OK || gf == gv)) ? c1 : 3);
+        // certify_lean is one-sided: true only where dp_certify says CERT_OK, same integer
+        typename fpx<T>::S gl = 0;
+        uint32_t ah = 0;
+        const bool lean = certify_lean(x, cert_params_for(T{}, A), &gl, &ah);
+        const bool agree = c1 == c2 && (c1 != CERT_OK || gf == gv) && (!lean || (c1 == CERT_OK && gl == gv));
+        out_cert[i] = (int8_t)(agree ? (c1 | (lean ? 4 : 0)) : -1);
         out_g[i] = (int64_t)gv;
     }
 }
