@@ -75,6 +75,12 @@ __host__ __device__ __forceinline__ uint32_t encode_stage_bytes(uint32_t chunk_n
     return (uint32_t)(tr::header + (tr::width + 7) / 8 + tr::width * nc + 32 + 15) & ~15u;
 }
 
+// compile-time bound of encode_stage_bytes over the chunk sizes a CTA of NT threads serves
+template <typename T, int NT>
+__host__ __device__ constexpr uint32_t encode_stage_bytes_max() {
+    return (uint32_t)(lane_traits<T>::header + (lane_traits<T>::width + 7) / 8 + lane_traits<T>::width * NT + 32 + 15) & ~15u;
+}
+
 // 32-bit word of lane values whose byte q is gathered (sb < 4: low word, else high)
 __device__ __forceinline__ uint32_t lane_word(uint64_t z, int sb) { return sb < 4 ? (uint32_t)z : (uint32_t)(z >> 32); }
 __device__ __forceinline__ uint32_t lane_word(uint32_t z, int) { return z; }
@@ -115,16 +121,18 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
     __shared__ uint32_t s_flag1[nwarps], s_flag2[nwarps];  // bit 31 exception | one-hot alphas
     __shared__ uint32_t s_mag[nwarps];                     // max floor_log10 + 1024 (0: none)
     __shared__ uint32_t s_warpw[nwarps];
-    __shared__ uint32_t s_rowinfo[64];       // plane p: dense << 31 | row offset in the image
+    __shared__ uint32_t s_rowoff[64];        // plane p: row offset in the image
     __shared__ uint32_t s_nzc[nwarps][16];   // 8-bit nonzero-byte counters, 4 planes/word
     __shared__ uint16_t s_wpre[64 * nwarps]; // nonzero bytes of plane p in warps before w
     __shared__ uint64_t s_dense;
     __shared__ uint32_t s_size;
     __shared__ B s_z1;
 
-    const uint32_t c = blockIdx.x;                 // < 2^31 chunks per launch
-    const uint32_t b = c / g.cpb;
-    const uint32_t ci = c - b * g.cpb;
+    // grid: x = chunk in batch, y + 65535 z = batch (no integer division)
+    const uint32_t b = blockIdx.y + 65535u * blockIdx.z;
+    const uint32_t ci = blockIdx.x;
+    if (b >= g.n_batches || ci >= g.chunks_in(b)) return;  // uniform per CTA
+    const uint32_t c = b * g.cpb + ci;                      // < 2^31 chunks per launch
     const uint64_t bcount = g.values_in(b);
     const uint64_t v0 = (uint64_t)b * g.batch_values + (uint64_t)ci * n;
     const uint64_t left = bcount - (uint64_t)ci * n;
@@ -152,10 +160,11 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
     // all-zero warp rows then need no store at all
     {
         uint4* st = reinterpret_cast<uint4*>(s_stage);
-        constexpr int kWords = 0;  // (runtime size below)
-        (void)kWords;
+        constexpr int kWords = (int)(encode_stage_bytes_max<T, NT>() >> 4);
         const int words = (int)(encode_stage_bytes<T>(n) >> 4);
-        for (int i = tid; i < words; i += PT) st[i] = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int i = tid; i < kWords; i += PT)
+            if (i < words) st[i] = make_uint4(0u, 0u, 0u, 0u);
     }
 
     // ---- analyze, phase 1: warp 0 runs the exact loop on 32 samples spread over the
@@ -223,12 +232,12 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
     if (!case2 && M != 0) {  // transform.hpp:62-65: beta_hat = alpha_max + floor_log10(max|v|) + 1
         int mag;
         if constexpr (sizeof(T) == 4) {
-            mag = floor_log10_bits((uint32_t)M);
+            mag = mag_of<T>(M);  // max|v| is a positive normal here (else Case 2)
         } else {
             // only the high word of max|v| is known: exact unless a decade boundary
             // falls inside it, then a second (uniform, rare) pass finds the low word
-            const int k0 = floor_log10_bits((uint64_t)M << 32);
-            const int k1 = floor_log10_bits((uint64_t)(((uint64_t)M << 32) | 0xffffffffu));
+            const int k0 = mag_of<T>((uint64_t)M << 32);
+            const int k1 = mag_of<T>(((uint64_t)M << 32) | 0xffffffffull);
             if (k0 == k1) {
                 mag = k0;
             } else {
@@ -248,7 +257,7 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
                 ml = 0;
 #pragma unroll
                 for (int i = 0; i < nwarps; ++i) ml = s_mag[i] > ml ? s_mag[i] : ml;
-                mag = floor_log10_bits(((uint64_t)M << 32) | ml);
+                mag = mag_of<T>(((uint64_t)M << 32) | ml);
             }
         }
         bhat = amax + mag + 1;
@@ -258,55 +267,70 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
     const uint32_t hB = case2 ? tr::exc_beta : (uint32_t)bhat;
 
     // ---- forward transform (transform.hpp:72-89) ----
+    // Case 1 at alpha_max == A0: every value has alpha_v <= A0, so v * 10^A0 lies within
+    // 3.5 ulp (<= 1/8) of its integer and rint == llround -- the certification's lane
+    // integers are final, also for the values the exact loop decided.  f64 lanes whose
+    // integers all fit in 30 bits (|v| < 2^(28 - e_p), e_p = exponent of the scale) take
+    // 32-bit delta/zigzag arithmetic: the same z, half the ALU work.
     const T scale = X::pow10(case2 ? 0 : amax);
-    bool range_err = false;
-    auto lane_g = [&](T x) -> B {
-        if (case2) return zigzag<B>(X::bits(x));
-        const T s = mul_rn(x, scale);
-        range_err |= !(fabs(s) < (T)0x1p62);  // numeric.hpp:153-154
-        return (B)(S)llround_away(s);
-    };
+    const bool reuse = !case2 && amax == A0;
+    const uint32_t lim = (2074u - ((uint32_t)__double2hiint((double)scale) >> 20)) << 20;
+    const bool narrow = sizeof(B) == 8 && __all_sync(0xffffffffu, reuse && mx < lim);
     B z[8];
     B orv = 0;
-    {
-        // Case 1 at alpha_max == A0: every value has alpha_v <= A0, so v * 10^A0 lies within
-        // 3.5 ulp (<= 1/8) of its integer and rint == llround -- the certification's lane
-        // integers are final, also for the values the exact loop decided
-        const bool reuse = !case2 && amax == A0;
-        const B gprev = lane_g(vprev);
-        if (tid == 0) s_z1 = gprev;
-        // f64 lanes whose integers all fit in 30 bits (|v| < 2^(28 - e_p), e_p = exponent
-        // of the scale) take 32-bit delta/zigzag arithmetic: same z, half the ALU work
-        const uint32_t lim = (2074u - ((uint32_t)__double2hiint((double)scale) >> 20)) << 20;
-        const bool narrow = sizeof(B) == 8 && __all_sync(0xffffffffu, reuse && mx < lim);
-        if (narrow) {
-            uint32_t gp = (uint32_t)gprev;
+    if (narrow) {
+        uint32_t gp = (uint32_t)__double2ll_rz(rint(mul_rn(vprev, scale)));
+        if (tid == 0) s_z1 = (B)(S)(int32_t)gp;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t gj = (uint32_t)gc[j];
+            const uint32_t d = gj - gp;
+            z[j] = (B)((d << 1) ^ (uint32_t)((int32_t)d >> 31));
+            gp = gj;
+        }
+        uint32_t o = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o |= (uint32_t)z[j];
+        orv = active ? (B)o : (B)0;
+    } else {
+        bool range_err = false;
+        auto lane_g = [&](T x) -> B {
+            if (case2) return zigzag<B>(X::bits(x));
+            const T s = mul_rn(x, scale);
+            range_err |= !(fabs(s) < (T)0x1p62);  // numeric.hpp:153-154
+            return (B)(S)llround_away(s);
+        };
+        B gp = lane_g(vprev);
+        if (tid == 0) s_z1 = gp;
+        if (reuse) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                const uint32_t gj = (uint32_t)gc[j];
-                const uint32_t d = gj - gp;
-                const uint32_t zz = (d << 1) ^ (uint32_t)((int32_t)d >> 31);
-                z[j] = active ? (B)zz : (B)0;
+                const B gj = (B)gc[j];
+                z[j] = zigzag<B>((B)(gj - gp));
                 gp = gj;
-                orv |= z[j];
             }
         } else {
-            B gp = gprev;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                const B gj = reuse ? (B)gc[j] : lane_g(v[j]);
-                z[j] = active ? zigzag<B>((B)(gj - gp)) : (B)0;
+                const B gj = lane_g(v[j]);
+                z[j] = zigzag<B>((B)(gj - gp));
                 gp = gj;
-                orv |= z[j];
             }
         }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) orv |= z[j];
+        if (!active) orv = 0;
+        if (range_err) record_error(ws.error, c, DEV_E_SCALE);
     }
-    if (range_err) record_error(ws.error, c, DEV_E_SCALE);
 
-    // ---- bit planes: warp-local width, 8x8 transposes -> s_planes, nonzero counts ----
+    // ---- bit planes: warp-local width, 8x8 transposes -> s_planes, nonzero counts.
+    //      Inactive columns (tid >= NC) are masked by orv = 0 only through warp_w; their
+    //      plane bytes are never stored. ----
     const int warp_w = bit_width(warp_or<B>(orv));
     const int nblk = (warp_w + 7) >> 3;
-    for (int sb = 0; sb < nblk; ++sb) {
+#pragma unroll
+    for (int sb = 0; sb < tr::width / 8; ++sb) {
+        if (sb >= nblk) break;
         // byte sb of lane j goes to byte 7-j of x: byte k of the transpose is then the row
         // byte of bit plane 8sb+k with lane j at bit 7-j (MSB-first, FORMAT.md:81-84)
         const uint32_t q = (uint32_t)(sb & 3);
@@ -315,7 +339,7 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
                                         __byte_perm(lane_word(z[5], sb), lane_word(z[4], sb), sel), 0x5410);
         const uint32_t xh = __byte_perm(__byte_perm(lane_word(z[3], sb), lane_word(z[2], sb), sel),
                                         __byte_perm(lane_word(z[1], sb), lane_word(z[0], sb), sel), 0x5410);
-        const uint64_t y = transpose8x8(((uint64_t)xh << 32) | xl);
+        const uint64_t y = active ? transpose8x8(((uint64_t)xh << 32) | xl) : 0ull;
         s_planes[sb * PT + tid] = y;
         // nonzero bytes per plane as 8-bit counters (<= 32 per warp, no carries)
         const uint32_t lo = __reduce_add_sync(0xffffffffu, nonzero_bytes((uint32_t)y));
@@ -369,8 +393,8 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
         const uint32_t tot1 = __shfl_sync(0xffffffffu, s1, 0);
         const uint32_t tot0 = __shfl_sync(0xffffffffu, s0, 0);
         const uint32_t base = HDR + fb;
-        s_rowinfo[lane + 32] = (base + (s1 - c1)) | (d1 ? 0x80000000u : 0u);
-        s_rowinfo[lane] = (base + tot1 + (s0 - c0)) | (d0 ? 0x80000000u : 0u);
+        s_rowoff[lane + 32] = base + (s1 - c1);
+        s_rowoff[lane] = base + tot1 + (s0 - c0);
         const uint32_t dm0 = __ballot_sync(0xffffffffu, d0);
         const uint32_t dm1 = __ballot_sync(0xffffffffu, d1);
         const uint32_t size = w ? base + tot1 + tot0 : (uint32_t)HDR;
@@ -397,23 +421,27 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
     }
     const uint32_t lt_mask = (1u << lane) - 1u;
     const int wblk = (w + 7) >> 3;
-    for (int sb = 0; sb < wblk; ++sb) {
+    uint8_t* const col = s_stage + tid;
+#pragma unroll
+    for (int sb = 0; sb < tr::width / 8; ++sb) {
+        if (sb >= wblk) break;
         const uint64_t y = sb < nblk ? s_planes[sb * PT + tid] : 0ull;  // above warp_w: zero
-        const int kmax = w - 8 * sb < 8 ? w - 8 * sb : 8;
-        if (kmax == 8 && ((dense >> (8 * sb)) & 0xffu) == 0xffu) {
+        const uint32_t ylo = (uint32_t)y, yhi = (uint32_t)(y >> 32);
+        const int kmax = w - 8 * sb;
+        const uint32_t dblk = (uint32_t)(dense >> (8 * sb)) & 0xffu;
+        if (kmax >= 8 && dblk == 0xffu) {
             // eight dense rows, consecutive in the image (plane 8sb+7 first): one base
             // address, immediate offsets
-            uint8_t* r7 = s_stage + (s_rowinfo[8 * sb + 7] & 0x7fffffffu) + tid;
+            uint8_t* r7 = col + s_rowoff[8 * sb + 7];
             if (active) {
-                const uint32_t lo = (uint32_t)y, hi = (uint32_t)(y >> 32);
-                r7[0 * NC] = (uint8_t)(hi >> 24);
-                r7[1 * NC] = (uint8_t)(hi >> 16);
-                r7[2 * NC] = (uint8_t)(hi >> 8);
-                r7[3 * NC] = (uint8_t)hi;
-                r7[4 * NC] = (uint8_t)(lo >> 24);
-                r7[5 * NC] = (uint8_t)(lo >> 16);
-                r7[6 * NC] = (uint8_t)(lo >> 8);
-                r7[7 * NC] = (uint8_t)lo;
+                r7[0 * NC] = (uint8_t)(yhi >> 24);
+                r7[1 * NC] = (uint8_t)(yhi >> 16);
+                r7[2 * NC] = (uint8_t)(yhi >> 8);
+                r7[3 * NC] = (uint8_t)yhi;
+                r7[4 * NC] = (uint8_t)(ylo >> 24);
+                r7[5 * NC] = (uint8_t)(ylo >> 16);
+                r7[6 * NC] = (uint8_t)(ylo >> 8);
+                r7[7 * NC] = (uint8_t)ylo;
             }
             continue;
         }
@@ -421,20 +449,19 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
         for (int k = 0; k < 8; ++k) {
             if (k >= kmax) break;
             const int p = 8 * sb + k;
-            const uint32_t info = s_rowinfo[p];
-            uint8_t* row = s_stage + (info & 0x7fffffffu);
-            const uint32_t byte = (uint32_t)(y >> (8 * k)) & 0xffu;
-            if (info >> 31) {
-                st_u8_if(active, row + tid, byte);
+            const uint32_t off = s_rowoff[p];
+            const uint32_t byte = (k < 4 ? ylo >> (8 * k) : yhi >> (8 * (k - 4))) & 0xffu;
+            if ((dblk >> k) & 1u) {
+                if (active) col[off] = (uint8_t)byte;
             } else {
-                // bitmap: byte j nonzero -> bit 7-j%8 of bitmap byte j/8; then the nonzero
-                // bytes in order (bitplane.hpp:126-148).  The buffer is zeroed: a warp whose
-                // 32 bytes are all zero writes nothing.
-                const uint32_t m = __ballot_sync(0xffffffffu, byte != 0);
+                // bitmap: byte j nonzero -> bit 7-j%8 of bitmap byte j/8 (lanes 0..3 write
+                // the warp's 4 bitmap bytes); then the nonzero bytes in order
+                // (bitplane.hpp:126-148).  The buffer is zeroed: a warp whose 32 bytes are
+                // all zero writes nothing.
+                const uint32_t m = __ballot_sync(0xffffffffu, byte != 0u);
                 if (m) {
-                    const uint32_t bm8 = __brev(m >> lane) >> 24;
-                    st_u8_if((lane & 7) == 0 && bm8 != 0, row + (tid >> 3), bm8);
-                    st_u8_if(byte != 0, row + BM + s_wpre[p * nwarps + warp] + __popc(m & lt_mask), byte);
+                    if (lane < 4 && 4 * warp + lane < BM) s_stage[off + 4 * warp + lane] = (uint8_t)(__brev(m >> (8 * lane)) >> 24);
+                    if (byte) s_stage[off + BM + s_wpre[p * nwarps + warp] + __popc(m & lt_mask)] = (uint8_t)byte;
                 }
             }
         }
@@ -445,7 +472,7 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
     uint4* dst = reinterpret_cast<uint4*>(ws.images + c * (uint64_t)ws.slot);
     const uint4* srcv = reinterpret_cast<const uint4*>(s_stage);
     const uint32_t nvec = (size + 15) >> 4;
-    for (uint32_t vv = tid; vv < nvec; vv += blockDim.x) dst[vv] = srcv[vv];
+    for (uint32_t vv = tid; vv < nvec; vv += NT) dst[vv] = srcv[vv];
 }
 
 // Placement: chunk images -> archive.  A tile of kPlaceTile consecutive chunks per CTA;
@@ -690,7 +717,8 @@ cudaError_t launch_encode(const T* d_in, const geometry& g, uint8_t* d_out, uint
     if (!kern) return cudaErrorInvalidConfiguration;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
     if (ev0 && (e = cudaEventRecord(ev0, st))) return e;
-    kern<<<(unsigned)g.n_chunks, threads, smem, st>>>(d_in, g, d_out, out_cap, ws);
+    const dim3 grid(g.cpb, (unsigned)(g.n_batches < 65535 ? g.n_batches : 65535), (unsigned)((g.n_batches + 65534) / 65535));
+    kern<<<grid, threads, smem, st>>>(d_in, g, d_out, out_cap, ws);
     if ((e = cudaGetLastError())) return e;
     if (ev1 && (e = cudaEventRecord(ev1, st))) return e;
     place_chunks_kernel<<<(unsigned)tiles, kPlaceTile, 0, st>>>(g, d_out, out_cap, ws, hdr);
