@@ -118,8 +118,13 @@ __device__ __forceinline__ bool near_integer(T s, T* N) {
 }
 
 // Reference loop (numeric.hpp:108-140) with (1) and (2).  alpha_v or -1 (exception).
-template <typename T>
-__device__ __noinline__ int dp_alpha_full(T v) {
+// K consecutive candidate scales are tested per step (independent multiply/round
+// chains: one step costs the latency of one candidate); the first candidate passing
+// the gap test decides, exactly as in the sequential loop.  K = 1 keeps the call-site
+// footprint small for the encoder's rare per-thread fallback; K = 4 is the latency-
+// bound sampling of phase 1.
+template <typename T, int K>
+__device__ __forceinline__ int dp_alpha_k(T v) {
     using X = fpx<T>;
     using B = typename X::B;
     const B b = X::bits(v);
@@ -131,13 +136,31 @@ __device__ __noinline__ int dp_alpha_full(T v) {
     int alpha = mag < 0 ? -mag : 0;
     const int lim0 = X::MAXB - 1 - mag;
     const int limit = lim0 < X::MAXA ? lim0 : X::MAXA;
-    for (; alpha <= limit; ++alpha) {
-        const T p = X::pow10(alpha);
-        T N;
-        if (near_integer<T>(mul_rn(v, p), &N)) return X::recon_ok(v, p, N) ? alpha : -1;
+    for (; alpha <= limit; alpha += K) {
+        T p[K], N[K];
+        bool near[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int a = alpha + k <= limit ? alpha + k : limit;
+            p[k] = X::pow10(a);
+            near[k] = alpha + k <= limit && near_integer<T>(mul_rn(v, p[k]), &N[k]);
+        }
+        // first passing candidate, selected without indexing (keeps p/N in registers)
+        int kk = -1;
+        T pk = p[0], Nk = N[0];
+#pragma unroll
+        for (int k = K - 1; k >= 0; --k) {
+            kk = near[k] ? k : kk;
+            pk = near[k] ? p[k] : pk;
+            Nk = near[k] ? N[k] : Nk;
+        }
+        if (kk >= 0) return X::recon_ok(v, pk, Nk) ? alpha + kk : -1;
     }
     return -1;
 }
+
+template <typename T>
+__device__ __noinline__ int dp_alpha_full(T v) { return dp_alpha_k<T, 1>(v); }
 
 enum : int { CERT_UNDECIDED = 0, CERT_OK = 1, CERT_EXC = 2 };
 

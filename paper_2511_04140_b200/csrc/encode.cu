@@ -121,9 +121,9 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
     __shared__ uint32_t s_flag1[nwarps], s_flag2[nwarps];  // bit 31 exception | one-hot alphas
     __shared__ uint32_t s_mag[nwarps];                     // max floor_log10 + 1024 (0: none)
     __shared__ uint32_t s_warpw[nwarps];
-    __shared__ uint32_t s_rowoff[64];        // plane p: row offset in the image
+    __shared__ __align__(16) uint32_t s_rowoff[64];        // plane p: row offset in the image
     __shared__ uint32_t s_nzc[nwarps][16];   // 8-bit nonzero-byte counters, 4 planes/word
-    __shared__ uint16_t s_wpre[64 * nwarps]; // nonzero bytes of plane p in warps before w
+    __shared__ __align__(16) uint16_t s_wpre[nwarps * 64]; // [w][p]: nonzero bytes of plane p in warps before w
     __shared__ uint64_t s_dense;
     __shared__ uint32_t s_size;
     __shared__ B s_z1;
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
     if (warp == 0) {
         const uint32_t si = (uint32_t)lane * (n >> 5) + (n >> 6);
         const T sv = si < len ? __ldg(in + v0 + si) : T(0);
-        const int a = dp_alpha_full<T>(sv);
+        const int a = dp_alpha_k<T, 4>(sv);
         const uint32_t f1 = __reduce_or_sync(0xffffffffu, a < 0 ? 0x80000000u : (1u << a));
         if (lane == 0) s_flag1[0] = f1;
     }
@@ -365,8 +365,8 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
             const int wq = (int)s_warpw[q];
             const uint32_t c0 = lane < wq ? (s_nzc[q][lane >> 2] >> (8 * (lane & 3))) & 0xffu : 0u;
             const uint32_t c1 = lane + 32 < wq ? (s_nzc[q][(lane + 32) >> 2] >> (8 * (lane & 3))) & 0xffu : 0u;
-            s_wpre[lane * nwarps + q] = (uint16_t)nz0;
-            s_wpre[(lane + 32) * nwarps + q] = (uint16_t)nz1;
+            s_wpre[q * 64 + lane] = (uint16_t)nz0;
+            s_wpre[q * 64 + lane + 32] = (uint16_t)nz1;
             nz0 += c0;
             nz1 += c1;
         }
@@ -428,8 +428,10 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
         const uint64_t y = sb < nblk ? s_planes[sb * PT + tid] : 0ull;  // above warp_w: zero
         const uint32_t ylo = (uint32_t)y, yhi = (uint32_t)(y >> 32);
         const int kmax = w - 8 * sb;
-        const uint32_t dblk = (uint32_t)(dense >> (8 * sb)) & 0xffu;
-        if (kmax >= 8 && dblk == 0xffu) {
+        const uint32_t valid = kmax >= 8 ? 0xffu : ((1u << kmax) - 1u);
+        const uint32_t dblk = (uint32_t)(dense >> (8 * sb)) & valid;
+        const uint32_t sblk = ~dblk & valid;
+        if (dblk == 0xffu) {
             // eight dense rows, consecutive in the image (plane 8sb+7 first): one base
             // address, immediate offsets
             uint8_t* r7 = col + s_rowoff[8 * sb + 7];
@@ -445,24 +447,41 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
             }
             continue;
         }
+        // this block's 8 row offsets and (sparse rows) this warp's payload prefixes
+        const uint4 o03 = *reinterpret_cast<const uint4*>(&s_rowoff[8 * sb]);
+        const uint4 o47 = *reinterpret_cast<const uint4*>(&s_rowoff[8 * sb + 4]);
+        const uint32_t off[8] = {o03.x, o03.y, o03.z, o03.w, o47.x, o47.y, o47.z, o47.w};
+        // remaining dense rows (a partly dense block is rare: uniform branches)
+        if (dblk) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            if (k >= kmax) break;
-            const int p = 8 * sb + k;
-            const uint32_t off = s_rowoff[p];
-            const uint32_t byte = (k < 4 ? ylo >> (8 * k) : yhi >> (8 * (k - 4))) & 0xffu;
-            if ((dblk >> k) & 1u) {
-                if (active) col[off] = (uint8_t)byte;
-            } else {
-                // bitmap: byte j nonzero -> bit 7-j%8 of bitmap byte j/8 (lanes 0..3 write
-                // the warp's 4 bitmap bytes); then the nonzero bytes in order
-                // (bitplane.hpp:126-148).  The buffer is zeroed: a warp whose 32 bytes are
-                // all zero writes nothing.
-                const uint32_t m = __ballot_sync(0xffffffffu, byte != 0u);
-                if (m) {
-                    if (lane < 4 && 4 * warp + lane < BM) s_stage[off + 4 * warp + lane] = (uint8_t)(__brev(m >> (8 * lane)) >> 24);
-                    if (byte) s_stage[off + BM + s_wpre[p * nwarps + warp] + __popc(m & lt_mask)] = (uint8_t)byte;
-                }
+            for (int k = 0; k < 8; ++k)
+                if (((dblk >> k) & 1u) && active) col[off[k]] = (uint8_t)(k < 4 ? ylo >> (8 * k) : yhi >> (8 * (k - 4)));
+        }
+        // sparse rows (bitplane.hpp:126-148): bitmap byte j nonzero -> bit 7-j%8 of bitmap
+        // byte j/8, then the nonzero bytes in order at warp prefix + ballot rank.  The 32
+        // bitmap bytes a warp owns in this block (8 planes x 4) go out in one store; the
+        // buffer is zeroed, so all-zero bytes are skipped.
+        if (sblk) {
+            const uint4 wp = *reinterpret_cast<const uint4*>(&s_wpre[warp * 64 + 8 * sb]);
+            const uint32_t wpre[8] = {wp.x & 0xffffu, wp.x >> 16, wp.y & 0xffffu, wp.y >> 16,
+                                      wp.z & 0xffffu, wp.z >> 16, wp.w & 0xffffu, wp.w >> 16};
+            uint32_t mk[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                mk[k] = __ballot_sync(0xffffffffu, ((k < 4 ? ylo >> (8 * k) : yhi >> (8 * (k - 4))) & 0xffu) != 0u);
+            {
+                const int kl = lane >> 2, ql = lane & 3;
+                uint32_t mm = mk[0];
+#pragma unroll
+                for (int k = 1; k < 8; ++k) mm = kl == k ? mk[k] : mm;
+                const uint32_t bm = __brev(mm >> (8 * ql)) >> 24;
+                if (((sblk >> kl) & 1u) && bm != 0u && 4 * warp + ql < BM) s_stage[s_rowoff[8 * sb + kl] + 4 * warp + ql] = (uint8_t)bm;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t byte = (k < 4 ? ylo >> (8 * k) : yhi >> (8 * (k - 4))) & 0xffu;
+                if (((sblk >> k) & 1u) && byte != 0u)
+                    s_stage[off[k] + BM + wpre[k] + __popc(mk[k] & lt_mask)] = (uint8_t)byte;
             }
         }
     }

@@ -19,7 +19,8 @@ __global__ void selftest_dp_kernel(const T* __restrict__ v, uint64_t n, int A, i
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const T x = v[i];
-        out_full[i] = (int8_t)dp_alpha_full<T>(x);
+        const int af = dp_alpha_full<T>(x);
+        out_full[i] = (int8_t)(dp_alpha_k<T, 4>(x) == af ? af : -2);  // -2: the 4-wide form disagrees
         out_lit[i] = (int8_t)dp_alpha<T>(x);
         typename fpx<T>::S gv = 0;
         const T p = fpx<T>::pow10(A);
