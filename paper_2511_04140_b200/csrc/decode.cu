@@ -196,7 +196,9 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
     __shared__ slot_meta s_meta[kDecodeSlots];
     __shared__ uint32_t s_code, s_w, s_hA;
     __shared__ B s_z1;
-    __shared__ uint32_t s_rowinfo[64];  // plane p: dense << 31 | row offset in the chunk
+    __shared__ __align__(16) uint32_t s_rowoff[64];        // plane p: row offset in the chunk
+    __shared__ __align__(16) uint16_t s_wpre[nwarps * 64];  // [warp][plane]: payload bytes of warps before
+    __shared__ uint64_t s_dmask;                            // bit p: plane p is dense
     __shared__ B s_wtot[nwarps];
 
     if (threadIdx.x == 0) {
@@ -269,6 +271,7 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
     // ===================== consumer warps =====================
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool active = tid < NC;
+    const uint32_t lt_mask = (1u << lane) - 1u;
     for (uint32_t it = 0;; ++it) {
         const int sl = (int)(it % kDecodeSlots);
         mbar_wait(&s_full[sl], (it / kDecodeSlots) & 1);
@@ -289,15 +292,16 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
             uint8_t* s_stage = smem + (size_t)sl * region;
             do {
     // ---- parse + validate in the reference's order (chunk_codec.hpp:92-117,
-    //      bitplane.hpp:160-186); warp 0 walks the rows, popcounts + warp prefixes
-    //      of sparse bitmaps in parallel ----
+    //      bitplane.hpp:160-186), warp 0.  Row offsets follow from the dense/sparse
+    //      flags and the sparse rows' bitmap popcounts (a chain over sparse rows only);
+    //      for each sparse row the per-warp payload prefixes are stored too. ----
     if (warp == 0) {
         const uint8_t* p = s_stage + a;
         // a chunk longer than any valid one cannot be staged: read its header from global
         const bool oversize = end > region;
         const uint8_t* hp = oversize ? arc + off : p;
         uint32_t code = 0, w = 0, hA = 0;
-        uint64_t flags = 0;
+        uint64_t flags = 0, dmask = 0;
         B z1 = 0;
         if (size < (uint32_t)HDR) {
             code = DEV_E_HDR_TRUNC;
@@ -342,6 +346,8 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
                 int bad = 64;                 // first row failing a truncation check
                 uint32_t bad_code = 0;
                 uint64_t sparse = ((uint64_t)sm1 << 32) | sm0;
+                // lane q < nwarps counts bitmap bytes [4q, 4q + 4) (consumer warp q's columns)
+                const uint32_t g0 = 4u * (uint32_t)lane;
                 while (sparse) {
                     const int r = __ffsll((long long)sparse) - 1;
                     sparse &= sparse - 1;
@@ -350,12 +356,23 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
                     const uint32_t rp = pos0 + nd * (uint32_t)NC + acc;
                     if (size < rp + (uint32_t)BM) { bad = r; bad_code = DEV_E_BITMAP_TRUNC; break; }
                     uint32_t pc = 0;
-                    for (int k = lane; k < BM; k += 32) pc += __popc(p[rp + k]);
-                    pc = __reduce_add_sync(0xffffffffu, pc);
-                    if (size - rp - (uint32_t)BM < pc) { bad = r; bad_code = DEV_E_PAYLOAD_TRUNC; break; }
-                    if (r0 > r) acc0 += (uint32_t)BM + pc;
-                    if (r1 > r) acc1 += (uint32_t)BM + pc;
-                    acc += (uint32_t)BM + pc;
+                    if (lane < nwarps) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (g0 + k < (uint32_t)BM) pc += __popc(p[rp + g0 + k]);
+                    }
+                    uint32_t incl = pc;  // inclusive scan over the (<= 16) groups
+#pragma unroll
+                    for (int d = 1; d < nwarps; d <<= 1) {
+                        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+                        if (lane >= d) incl += t;
+                    }
+                    const uint32_t tot = __shfl_sync(0xffffffffu, incl, nwarps - 1);
+                    if (lane < nwarps) s_wpre[lane * 64 + (w - 1 - r)] = (uint16_t)(incl - pc);
+                    if (size - rp - (uint32_t)BM < tot) { bad = r; bad_code = DEV_E_PAYLOAD_TRUNC; break; }
+                    if (r0 > r) acc0 += (uint32_t)BM + tot;
+                    if (r1 > r) acc1 += (uint32_t)BM + tot;
+                    acc += (uint32_t)BM + tot;
                 }
                 const uint32_t pr0 = pos0 + nd0 * (uint32_t)NC + acc0;
                 const uint32_t pr1 = pos0 + nd1 * (uint32_t)NC + acc1;
@@ -365,8 +382,9 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
                 if (t0 | t1) code = DEV_E_ROW_TRUNC;
                 else if (bad_code) code = bad_code;
                 else if (pos0 + (uint32_t)(__popc(dm0) + __popc(dm1)) * (uint32_t)NC + acc != size) code = DEV_E_SIZE;
-                if (v0r) s_rowinfo[w - 1 - r0] = pr0 | (d0 ? 0x80000000u : 0u);
-                if (v1r) s_rowinfo[w - 1 - r1] = pr1 | (d1 ? 0x80000000u : 0u);
+                if (v0r) s_rowoff[w - 1 - r0] = pr0;
+                if (v1r) s_rowoff[w - 1 - r1] = pr1;
+                dmask = flags;  // flag bit (w-1-r) marks row r = plane w-1-r: bit p <-> plane p
             } else if (!code && pos != size) {
                 code = DEV_E_SIZE;
             }
@@ -376,6 +394,7 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
             s_w = w;
             s_hA = hA;
             s_z1 = z1;
+            s_dmask = dmask;
         }
     }
     consumer_sync<NT>();
@@ -386,45 +405,83 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
     const int w = (int)s_w;
     const uint32_t hA = s_hA;
     const bool case2 = hA > (uint32_t)tr::max_alpha;
+    const uint64_t dmask = s_dmask;
 
     // ---- planes -> lanes: thread t gathers byte t of every row (dense: verbatim;
-    //      sparse: bitmap bit t, payload byte at warp prefix + ballot rank), then
-    //      8x8 transposes rebuild lanes 8t..8t+7 ----
+    //      sparse: bitmap bit t, payload byte at warp prefix + ballot rank), one 8x8
+    //      transpose per 8 planes, then a byte transpose assembles the lanes ----
     const uint8_t* img = s_stage + a;
-    const uint32_t lt_mask = (1u << lane) - 1u;
-    B z[8];
+    uint64_t yb[W / 8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) z[j] = 0;
+    for (int sb = 0; sb < W / 8; ++sb) yb[sb] = 0;
     const int nblk = (w + 7) >> 3;
-    for (int sb = 0; sb < nblk; ++sb) {
+#pragma unroll
+    for (int sb = 0; sb < W / 8; ++sb) {
+        if (sb >= nblk) break;
+        const uint4 o03 = *reinterpret_cast<const uint4*>(&s_rowoff[8 * sb]);
+        const uint4 o47 = *reinterpret_cast<const uint4*>(&s_rowoff[8 * sb + 4]);
+        const uint32_t ro[8] = {o03.x, o03.y, o03.z, o03.w, o47.x, o47.y, o47.z, o47.w};
+        const int kmax = w - 8 * sb;
+        const uint32_t valid = kmax >= 8 ? 0xffu : ((1u << kmax) - 1u);
+        const uint32_t dblk = (uint32_t)(dmask >> (8 * sb)) & valid;
         uint32_t xb[8];
+        if (dblk == 0xffu) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int p = 8 * sb + k;
-            uint32_t byte = 0;
-            if (p < w) {
-                const uint32_t info = s_rowinfo[p];
-                const uint8_t* row = img + (info & 0x7fffffffu);
-                if (info >> 31) {
-                    if (active) byte = row[tid];
-                } else {
-                    // payload bytes of the warps before this one, then the ballot rank
-                    uint32_t pc = 0;
-                    for (int k = lane; k < 4 * warp && k < BM; k += 32) pc += __popc(row[k]);
-                    const uint32_t pre = __reduce_add_sync(0xffffffffu, pc);
-                    const uint32_t bit = active ? (row[tid >> 3] >> (7 - (tid & 7))) & 1u : 0u;
-                    const uint32_t m = __ballot_sync(0xffffffffu, bit);
-                    if (bit) byte = row[BM + pre + __popc(m & lt_mask)];
-                }
+            for (int k = 0; k < 8; ++k) xb[k] = active ? img[ro[k] + tid] : 0u;
+        } else {
+            const uint4 wp = *reinterpret_cast<const uint4*>(&s_wpre[warp * 64 + 8 * sb]);
+            const uint32_t wpre[8] = {wp.x & 0xffffu, wp.x >> 16, wp.y & 0xffffu, wp.y >> 16,
+                                      wp.z & 0xffffu, wp.z >> 16, wp.w & 0xffffu, wp.w >> 16};
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const bool vk = (valid >> k) & 1u, dk = (dblk >> k) & 1u;
+                const uint32_t bmb = (vk && !dk && active) ? img[ro[k] + (tid >> 3)] : 0u;
+                const uint32_t bit = (bmb >> (7 - (tid & 7))) & 1u;
+                const uint32_t m = __ballot_sync(0xffffffffu, bit);
+                const uint32_t idx = dk ? ro[k] + tid : ro[k] + BM + wpre[k] + __popc(m & lt_mask);
+                xb[k] = ((dk && active) || bit) ? img[idx] : 0u;
             }
-            xb[k] = byte;
         }
-        const uint32_t xl = xb[0] | (xb[1] << 8) | (xb[2] << 16) | (xb[3] << 24);
-        const uint32_t xh = xb[4] | (xb[5] << 8) | (xb[6] << 16) | (xb[7] << 24);
-        const uint64_t y = transpose8x8(((uint64_t)xh << 32) | xl);
-        // byte 7-j of y is byte sb of lane j
+        // byte k of x = row byte of plane 8sb+k (xb[k] <= 0xff: selector 7 reads a zero byte)
+        const uint32_t xl = __byte_perm(xb[0], xb[1], 0x7740) | __byte_perm(xb[2], xb[3], 0x4077);
+        const uint32_t xh = __byte_perm(xb[4], xb[5], 0x7740) | __byte_perm(xb[6], xb[7], 0x4077);
+        yb[sb] = transpose8x8(((uint64_t)xh << 32) | xl);  // byte 7-j = byte sb of lane j
+    }
+    // byte transpose: lane j's byte sb = byte 7-j of yb[sb]
+    B z[8];
+    {
+        auto tr4 = [](uint32_t h0, uint32_t h1, uint32_t h2, uint32_t h3, uint32_t o[4]) {
+            // o[q] = [h0.b(q), h1.b(q), h2.b(q), h3.b(q)]
+            const uint32_t p01l = __byte_perm(h0, h1, 0x5140), p01h = __byte_perm(h0, h1, 0x7362);
+            const uint32_t p23l = __byte_perm(h2, h3, 0x5140), p23h = __byte_perm(h2, h3, 0x7362);
+            o[0] = __byte_perm(p01l, p23l, 0x5410);
+            o[1] = __byte_perm(p01l, p23l, 0x7632);
+            o[2] = __byte_perm(p01h, p23h, 0x5410);
+            o[3] = __byte_perm(p01h, p23h, 0x7632);
+        };
+        uint32_t lo[8], hi[8];
+        uint32_t q[4];
+        // low lane words: blocks 0..3; lane j = 7 - byte index
+        tr4((uint32_t)(yb[0] >> 32), (uint32_t)(yb[1] >> 32), (uint32_t)(yb[2] >> 32), (uint32_t)(yb[3] >> 32), q);
+        lo[3] = q[0]; lo[2] = q[1]; lo[1] = q[2]; lo[0] = q[3];
+        tr4((uint32_t)yb[0], (uint32_t)yb[1], (uint32_t)yb[2], (uint32_t)yb[3], q);
+        lo[7] = q[0]; lo[6] = q[1]; lo[5] = q[2]; lo[4] = q[3];
+        if constexpr (W == 64) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) z[j] |= (B)((y >> (8 * (7 - j))) & 0xffu) << (8 * sb);
+            for (int j = 0; j < 8; ++j) hi[j] = 0;
+            if (nblk > 4) {
+                tr4((uint32_t)(yb[4] >> 32), (uint32_t)(yb[5] >> 32), (uint32_t)(yb[6] >> 32), (uint32_t)(yb[7] >> 32), q);
+                hi[3] = q[0]; hi[2] = q[1]; hi[1] = q[2]; hi[0] = q[3];
+                tr4((uint32_t)yb[4], (uint32_t)yb[5], (uint32_t)yb[6], (uint32_t)yb[7], q);
+                hi[7] = q[0]; hi[6] = q[1]; hi[5] = q[2]; hi[4] = q[3];
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) z[j] = (B)(((uint64_t)hi[j] << 32) | lo[j]);
+        } else {
+            (void)hi;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) z[j] = (B)lo[j];
+        }
     }
 
     // ---- inverse transform: wrapping inclusive scan (transform.hpp:97-100) ----
