@@ -154,10 +154,6 @@ __device__ __forceinline__ void consumer_sync() {
 
 constexpr int kDecodeSlots = 3;
 enum : uint32_t { SLOT_CHUNK = 0, SLOT_SKIP = 1, SLOT_EXIT = 2 };
-struct slot_meta {
-    uint64_t off;
-    uint32_t chunk, size, kind;
-};
 
 template <typename T>
 __host__ __device__ __forceinline__ uint32_t decode_region_bytes(uint32_t chunk_n) {
@@ -166,11 +162,134 @@ __host__ __device__ __forceinline__ uint32_t decode_region_bytes(uint32_t chunk_
     return (uint32_t)(tr::header + (tr::width + 7) / 8 + tr::width * nc + 16 + 15) & ~15u;
 }
 
+// Everything the consumers need about one staged chunk, written by the producer warp.
+template <typename B, int NW>
+struct __align__(16) slot_info {
+    uint32_t rowoff[64];      // plane p: row offset from the chunk's first byte
+    uint16_t wpre[NW * 64];   // [warp][plane]: sparse payload bytes of the warps before
+    uint64_t dmask;           // bit p: plane p is dense
+    uint64_t off;             // archive offset of the chunk
+    B z1;
+    B wtot[NW];               // consumer scan scratch
+    uint32_t chunk, size, kind, code, w, hA;
+};
+
+// Parse + validate one staged chunk in the reference's order (chunk_codec.hpp:92-117,
+// bitplane.hpp:160-186), one warp.  Row offsets follow from the dense/sparse flags
+// and the sparse rows' bitmap popcounts (a chain over sparse rows only); for each
+// sparse row the consumer warps' payload prefixes are stored too.
+template <typename T, int NW, typename SI>
+__device__ __forceinline__ void parse_chunk(const uint8_t* p, const uint8_t* hp, uint32_t size, bool oversize,
+                                            int NC, int BM, SI& si, int lane) {
+    using tr = lane_traits<T>;
+    using B = typename tr::B;
+    constexpr int W = tr::width;
+    constexpr int HDR = tr::header;
+    uint32_t code = 0, w = 0, hA = 0;
+    uint64_t flags = 0, dmask = 0;
+    B z1 = 0;
+    if (size < (uint32_t)HDR) {
+        code = DEV_E_HDR_TRUNC;
+    } else {
+        hA = hp[0];
+        const uint32_t hB = hp[1];
+        const bool case2 = hA > (uint32_t)tr::max_alpha || hB > (uint32_t)tr::max_beta;
+        if (case2 && !(hA == (uint32_t)tr::exc_alpha && hB == (uint32_t)tr::exc_beta)) code = DEV_E_META;
+        if (!code) {
+#pragma unroll
+            for (int i = 0; i < (int)sizeof(B); ++i) z1 |= (B)hp[2 + i] << (8 * i);
+            w = hp[2 + sizeof(B)];
+            if (w > (uint32_t)W) code = DEV_E_W;
+        }
+        uint32_t pos = HDR;
+        if (!code && w > 0) {
+            const uint32_t fb = (w + 7) / 8;
+            if (size - pos < fb) {
+                code = DEV_E_FLAGS_TRUNC;
+            } else {
+                for (uint32_t i = 0; i < fb; ++i) flags = flags << 8 | hp[pos + i];
+                if (fb * 8 > w && (flags >> w) != 0) code = DEV_E_FLAG_PAD;
+                pos += fb;
+            }
+        }
+        if (!code && oversize) code = DEV_E_SIZE;  // no valid chunk of this geometry is that long
+        if (!code && w > 0) {
+            // Row walk (bitplane.hpp:160-186).  Row r (plane w-1-r) sits at
+            //   pos0 + NC * #dense rows before r + sum over sparse rows before r of (BM + popcount)
+            // Lane L owns rows L and L+32; only the sparse rows' popcounts are sequential.
+            const uint32_t pos0 = pos;
+            const int r0 = lane, r1 = lane + 32;
+            const bool v0r = r0 < (int)w, v1r = r1 < (int)w;
+            const bool d0 = v0r && ((flags >> (w - 1 - r0)) & 1);
+            const bool d1 = v1r && ((flags >> (w - 1 - r1)) & 1);
+            const uint32_t dm0 = __ballot_sync(0xffffffffu, d0), dm1 = __ballot_sync(0xffffffffu, d1);
+            const uint32_t sm0 = __ballot_sync(0xffffffffu, v0r && !d0), sm1 = __ballot_sync(0xffffffffu, v1r && !d1);
+            const uint32_t lt = (1u << lane) - 1u;
+            const uint32_t nd0 = __popc(dm0 & lt), nd1 = __popc(dm0) + __popc(dm1 & lt);
+            uint32_t acc0 = 0, acc1 = 0;  // sparse bytes before rows r0 / r1
+            uint32_t acc = 0;             // sparse bytes so far
+            int bad = 64;                 // first row failing a truncation check
+            uint32_t bad_code = 0;
+            uint64_t sparse = ((uint64_t)sm1 << 32) | sm0;
+            // lane q < NW counts bitmap bytes [4q, 4q + 4) (consumer warp q's columns)
+            const uint32_t g0 = 4u * (uint32_t)lane;
+            while (sparse) {
+                const int r = __ffsll((long long)sparse) - 1;
+                sparse &= sparse - 1;
+                const uint32_t nd = r < 32 ? __popc(dm0 & ((1u << r) - 1u))
+                                           : __popc(dm0) + __popc(dm1 & ((1u << (r - 32)) - 1u));
+                const uint32_t rp = pos0 + nd * (uint32_t)NC + acc;
+                if (size < rp + (uint32_t)BM) { bad = r; bad_code = DEV_E_BITMAP_TRUNC; break; }
+                uint32_t pc = 0;
+                if (lane < NW) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (g0 + k < (uint32_t)BM) pc += __popc(p[rp + g0 + k]);
+                }
+                uint32_t incl = pc;  // inclusive scan over the (<= 16) groups
+#pragma unroll
+                for (int d = 1; d < NW; d <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += t;
+                }
+                const uint32_t tot = __shfl_sync(0xffffffffu, incl, NW - 1);
+                if (lane < NW) si.wpre[lane * 64 + (w - 1 - r)] = (uint16_t)(incl - pc);
+                if (size - rp - (uint32_t)BM < tot) { bad = r; bad_code = DEV_E_PAYLOAD_TRUNC; break; }
+                if (r0 > r) acc0 += (uint32_t)BM + tot;
+                if (r1 > r) acc1 += (uint32_t)BM + tot;
+                acc += (uint32_t)BM + tot;
+            }
+            const uint32_t pr0 = pos0 + nd0 * (uint32_t)NC + acc0;
+            const uint32_t pr1 = pos0 + nd1 * (uint32_t)NC + acc1;
+            // dense rows truncated before the first sparse failure (reference order)
+            const uint32_t t0 = __ballot_sync(0xffffffffu, d0 && r0 < bad && size - pr0 < (uint32_t)NC);
+            const uint32_t t1 = __ballot_sync(0xffffffffu, d1 && r1 < bad && size - pr1 < (uint32_t)NC);
+            if (t0 | t1) code = DEV_E_ROW_TRUNC;
+            else if (bad_code) code = bad_code;
+            else if (pos0 + (uint32_t)(__popc(dm0) + __popc(dm1)) * (uint32_t)NC + acc != size) code = DEV_E_SIZE;
+            if (v0r) si.rowoff[w - 1 - r0] = pr0;
+            if (v1r) si.rowoff[w - 1 - r1] = pr1;
+            dmask = flags;  // flag bit (w-1-r) marks row r = plane w-1-r: bit p <-> plane p
+        } else if (!code && pos != size) {
+            code = DEV_E_SIZE;
+        }
+    }
+    if (lane == 0) {
+        si.code = code;
+        si.w = w;
+        si.hA = hA;
+        si.z1 = z1;
+        si.dmask = dmask;
+    }
+}
+
 // Persistent, warp-specialized decode.  Block 0 is the frame walker.  In every other
-// block the last warp is a producer: it takes chunk tickets, waits for the walker to
-// publish the chunk's batch, and streams the chunk bytes (16-B cp.async at the source's
-// 16-B phase) into a ring of kDecodeSlots smem slots; the other NT threads consume the
-// slots in order, so staging of chunk i+1, i+2 overlaps the decode of chunk i.
+// block the last warp is the producer: it takes chunk tickets, waits for the walker to
+// publish the chunk's batch, streams the chunk bytes (16-B cp.async at the source's
+// 16-B phase) into a ring of kDecodeSlots smem slots, parses and validates the staged
+// chunk, and hands the slot to the NT consumer threads, which only gather, scan and
+// store.  Staging and parsing of chunk i+1, i+2 overlap the decode of chunk i; the next
+// ticket's offsets are fetched while the current copy is in flight.
 template <typename T, int NT>
 __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* __restrict__ arc, uint64_t len,
                                                                 geometry g, T* __restrict__ out,
@@ -179,8 +298,8 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
     using B = typename tr::B;
     using S = typename tr::S;
     constexpr int W = tr::width;
-    constexpr int HDR = tr::header;
     constexpr int nwarps = NT / 32;
+    using SI = slot_info<B, nwarps>;
 
     if (blockIdx.x == 0) {
         walk_frames(arc, len, g, ws);
@@ -193,18 +312,12 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
     const uint32_t region = decode_region_bytes<T>(n);
 
     __shared__ __align__(8) uint64_t s_full[kDecodeSlots], s_empty[kDecodeSlots];
-    __shared__ slot_meta s_meta[kDecodeSlots];
-    __shared__ uint32_t s_code, s_w, s_hA;
-    __shared__ B s_z1;
-    __shared__ __align__(16) uint32_t s_rowoff[64];        // plane p: row offset in the chunk
-    __shared__ __align__(16) uint16_t s_wpre[nwarps * 64];  // [warp][plane]: payload bytes of warps before
-    __shared__ uint64_t s_dmask;                            // bit p: plane p is dense
-    __shared__ B s_wtot[nwarps];
+    __shared__ SI s_info[kDecodeSlots];
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kDecodeSlots; ++i) {
-            mbar_init(&s_full[i], 64);   // 32 copy-completion + 32 release arrivals
-            mbar_init(&s_empty[i], 1);
+            mbar_init(&s_full[i], 32);       // every producer lane
+            mbar_init(&s_empty[i], nwarps);  // one per consumer warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -214,15 +327,14 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
         // ===================== producer warp =====================
         const int lane = threadIdx.x & 31;
         const bool aligned = ((uintptr_t)arc & 15) == 0;
-        for (uint32_t it = 0;; ++it) {
-            const int sl = (int)(it % kDecodeSlots);
-            if (it >= (uint32_t)kDecodeSlots) mbar_wait(&s_empty[sl], ((it / kDecodeSlots) & 1) ^ 1);
-            uint32_t t = 0;
+        // next ticket: chunk index, kind, archive offset and size (lane 0 fetches)
+        auto fetch = [&](uint32_t& t, uint32_t& kind, uint64_t& off, uint32_t& size) {
+            t = 0;
+            kind = SLOT_CHUNK;
+            off = 0;
+            size = 0;
             if (lane == 0) t = atomicAdd(ws.ticket, 1u);
             t = __shfl_sync(0xffffffffu, t, 0);
-            uint32_t kind = SLOT_CHUNK;
-            uint64_t off = 0;
-            uint32_t size = 0;
             if (t >= g.n_chunks) {
                 kind = SLOT_EXIT;
             } else if (lane == 0) {
@@ -242,28 +354,51 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
             kind = __shfl_sync(0xffffffffu, kind, 0);
             off = __shfl_sync(0xffffffffu, off, 0);
             size = __shfl_sync(0xffffffffu, size, 0);
+        };
+        uint32_t t, kind, size;
+        uint64_t off;
+        fetch(t, kind, off, size);
+        for (uint32_t it = 0;; ++it) {
+            const int sl = (int)(it % kDecodeSlots);
+            if (it >= (uint32_t)kDecodeSlots) mbar_wait(&s_empty[sl], ((it / kDecodeSlots) & 1) ^ 1);
+            SI& si = s_info[sl];
             uint8_t* buf = smem + (size_t)sl * region;
-            if (kind == SLOT_CHUNK) {
-                const uint32_t a = (uint32_t)(off & 15);
+            const uint32_t a = (uint32_t)(off & 15);
+            const uint32_t end = a + size;
+            const bool staged = kind == SLOT_CHUNK && end <= region;
+            if (staged) {
                 const uint64_t base = off - a;
-                const uint32_t end = a + size;
-                if (end <= region) {
-                    const uint32_t nvec = (end + 15) >> 4;
-                    for (uint32_t vv = lane; vv < nvec; vv += 32) {
-                        const uint64_t gaddr = base + 16ull * vv;
-                        if (aligned && gaddr + 16 <= len) {
-                            cp_async16(buf + 16 * vv, arc + gaddr);
-                        } else {  // ragged archive end: plain byte copies
-                            for (uint32_t k = 0; k < 16; ++k)
-                                if (gaddr + k < len) buf[16 * vv + k] = arc[gaddr + k];
-                        }
+                const uint32_t nvec = (end + 15) >> 4;
+                for (uint32_t vv = lane; vv < nvec; vv += 32) {
+                    const uint64_t gaddr = base + 16ull * vv;
+                    if (aligned && gaddr + 16 <= len) {
+                        cp_async16(buf + 16 * vv, arc + gaddr);
+                    } else {  // ragged archive end: plain byte copies
+                        for (uint32_t k = 0; k < 16; ++k)
+                            if (gaddr + k < len) buf[16 * vv + k] = arc[gaddr + k];
                     }
                 }
             }
-            if (lane == 0) s_meta[sl] = slot_meta{off, t, size, kind};
-            cp_async_arrive(&s_full[sl]);
+            // the next ticket's offsets load while the copy is in flight
+            uint32_t t2 = 0, kind2 = SLOT_EXIT, size2 = 0;
+            uint64_t off2 = 0;
+            if (kind != SLOT_EXIT) fetch(t2, kind2, off2, size2);
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();
+            if (kind == SLOT_CHUNK) parse_chunk<T, nwarps>(buf + a, staged ? buf + a : arc + off, size, !staged, NC, BM, si, lane);
+            if (lane == 0) {
+                si.kind = kind;
+                si.chunk = t;
+                si.off = off;
+                si.size = size;
+            }
+            __syncwarp();
             mbar_arrive(&s_full[sl]);
             if (kind == SLOT_EXIT) break;
+            t = t2;
+            kind = kind2;
+            off = off2;
+            size = size2;
         }
         return;
     }
@@ -275,142 +410,30 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
     for (uint32_t it = 0;; ++it) {
         const int sl = (int)(it % kDecodeSlots);
         mbar_wait(&s_full[sl], (it / kDecodeSlots) & 1);
-        const slot_meta meta = s_meta[sl];
-        if (meta.kind == SLOT_EXIT) break;
-        if (meta.kind == SLOT_CHUNK) {
-            const uint32_t c = meta.chunk;
+        SI& si = s_info[sl];
+        const uint32_t kind = si.kind;
+        if (kind == SLOT_EXIT) break;
+        const uint32_t code = kind == SLOT_CHUNK ? si.code : 0u;
+        if (kind == SLOT_CHUNK && code != 0u) {
+            if (tid == 0) record_error(ws.error, si.chunk, code);
+        } else if (kind == SLOT_CHUNK) {
+            const uint32_t c = si.chunk;
             const uint32_t b = c / g.cpb;
             const uint32_t ci = c - b * g.cpb;
             const uint64_t bcount = g.values_in(b);
             const uint64_t v0 = (uint64_t)b * g.batch_values + (uint64_t)ci * n;
             const uint64_t left = bcount - (uint64_t)ci * n;
             const uint32_t count = left < n ? (uint32_t)left : n;
-            const uint64_t off = meta.off;
-            const uint32_t size = meta.size;
-            const uint32_t a = (uint32_t)(off & 15);
-            const uint32_t end = a + size;
-            uint8_t* s_stage = smem + (size_t)sl * region;
-            do {
-    // ---- parse + validate in the reference's order (chunk_codec.hpp:92-117,
-    //      bitplane.hpp:160-186), warp 0.  Row offsets follow from the dense/sparse
-    //      flags and the sparse rows' bitmap popcounts (a chain over sparse rows only);
-    //      for each sparse row the per-warp payload prefixes are stored too. ----
-    if (warp == 0) {
-        const uint8_t* p = s_stage + a;
-        // a chunk longer than any valid one cannot be staged: read its header from global
-        const bool oversize = end > region;
-        const uint8_t* hp = oversize ? arc + off : p;
-        uint32_t code = 0, w = 0, hA = 0;
-        uint64_t flags = 0, dmask = 0;
-        B z1 = 0;
-        if (size < (uint32_t)HDR) {
-            code = DEV_E_HDR_TRUNC;
-        } else {
-            hA = hp[0];
-            const uint32_t hB = hp[1];
-            const bool case2 = hA > (uint32_t)tr::max_alpha || hB > (uint32_t)tr::max_beta;
-            if (case2 && !(hA == (uint32_t)tr::exc_alpha && hB == (uint32_t)tr::exc_beta)) code = DEV_E_META;
-            if (!code) {
-#pragma unroll
-                for (int i = 0; i < (int)sizeof(B); ++i) z1 |= (B)hp[2 + i] << (8 * i);
-                w = hp[2 + sizeof(B)];
-                if (w > (uint32_t)W) code = DEV_E_W;
-            }
-            uint32_t pos = HDR;
-            if (!code && w > 0) {
-                const uint32_t fb = (w + 7) / 8;
-                if (size - pos < fb) {
-                    code = DEV_E_FLAGS_TRUNC;
-                } else {
-                    for (uint32_t i = 0; i < fb; ++i) flags = flags << 8 | hp[pos + i];
-                    if (fb * 8 > w && (flags >> w) != 0) code = DEV_E_FLAG_PAD;
-                    pos += fb;
-                }
-            }
-            if (!code && oversize) code = DEV_E_SIZE;  // no valid chunk of this geometry is that long
-            if (!code && w > 0) {
-                // Row walk (bitplane.hpp:160-186).  Row r (plane w-1-r) sits at
-                //   pos0 + NC * #dense rows before r + sum over sparse rows before r of (BM + popcount)
-                // Lane L owns rows L and L+32; only the sparse rows' popcounts are sequential.
-                const uint32_t pos0 = pos;
-                const int r0 = lane, r1 = lane + 32;
-                const bool v0r = r0 < (int)w, v1r = r1 < (int)w;
-                const bool d0 = v0r && ((flags >> (w - 1 - r0)) & 1);
-                const bool d1 = v1r && ((flags >> (w - 1 - r1)) & 1);
-                const uint32_t dm0 = __ballot_sync(0xffffffffu, d0), dm1 = __ballot_sync(0xffffffffu, d1);
-                const uint32_t sm0 = __ballot_sync(0xffffffffu, v0r && !d0), sm1 = __ballot_sync(0xffffffffu, v1r && !d1);
-                const uint32_t lt = (1u << lane) - 1u;
-                const uint32_t nd0 = __popc(dm0 & lt), nd1 = __popc(dm0) + __popc(dm1 & lt);
-                uint32_t acc0 = 0, acc1 = 0;  // sparse bytes before rows r0 / r1
-                uint32_t acc = 0;             // sparse bytes so far
-                int bad = 64;                 // first row failing a truncation check
-                uint32_t bad_code = 0;
-                uint64_t sparse = ((uint64_t)sm1 << 32) | sm0;
-                // lane q < nwarps counts bitmap bytes [4q, 4q + 4) (consumer warp q's columns)
-                const uint32_t g0 = 4u * (uint32_t)lane;
-                while (sparse) {
-                    const int r = __ffsll((long long)sparse) - 1;
-                    sparse &= sparse - 1;
-                    const uint32_t nd = r < 32 ? __popc(dm0 & ((1u << r) - 1u))
-                                               : __popc(dm0) + __popc(dm1 & ((1u << (r - 32)) - 1u));
-                    const uint32_t rp = pos0 + nd * (uint32_t)NC + acc;
-                    if (size < rp + (uint32_t)BM) { bad = r; bad_code = DEV_E_BITMAP_TRUNC; break; }
-                    uint32_t pc = 0;
-                    if (lane < nwarps) {
-#pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            if (g0 + k < (uint32_t)BM) pc += __popc(p[rp + g0 + k]);
-                    }
-                    uint32_t incl = pc;  // inclusive scan over the (<= 16) groups
-#pragma unroll
-                    for (int d = 1; d < nwarps; d <<= 1) {
-                        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
-                        if (lane >= d) incl += t;
-                    }
-                    const uint32_t tot = __shfl_sync(0xffffffffu, incl, nwarps - 1);
-                    if (lane < nwarps) s_wpre[lane * 64 + (w - 1 - r)] = (uint16_t)(incl - pc);
-                    if (size - rp - (uint32_t)BM < tot) { bad = r; bad_code = DEV_E_PAYLOAD_TRUNC; break; }
-                    if (r0 > r) acc0 += (uint32_t)BM + tot;
-                    if (r1 > r) acc1 += (uint32_t)BM + tot;
-                    acc += (uint32_t)BM + tot;
-                }
-                const uint32_t pr0 = pos0 + nd0 * (uint32_t)NC + acc0;
-                const uint32_t pr1 = pos0 + nd1 * (uint32_t)NC + acc1;
-                // dense rows truncated before the first sparse failure (reference order)
-                const uint32_t t0 = __ballot_sync(0xffffffffu, d0 && r0 < bad && size - pr0 < (uint32_t)NC);
-                const uint32_t t1 = __ballot_sync(0xffffffffu, d1 && r1 < bad && size - pr1 < (uint32_t)NC);
-                if (t0 | t1) code = DEV_E_ROW_TRUNC;
-                else if (bad_code) code = bad_code;
-                else if (pos0 + (uint32_t)(__popc(dm0) + __popc(dm1)) * (uint32_t)NC + acc != size) code = DEV_E_SIZE;
-                if (v0r) s_rowoff[w - 1 - r0] = pr0;
-                if (v1r) s_rowoff[w - 1 - r1] = pr1;
-                dmask = flags;  // flag bit (w-1-r) marks row r = plane w-1-r: bit p <-> plane p
-            } else if (!code && pos != size) {
-                code = DEV_E_SIZE;
-            }
-        }
-        if (lane == 0) {
-            s_code = code;
-            s_w = w;
-            s_hA = hA;
-            s_z1 = z1;
-            s_dmask = dmask;
-        }
-    }
-    consumer_sync<NT>();
-    if (s_code) {
-        if (tid == 0) record_error(ws.error, c, s_code);
-        break;
-    }
-    const int w = (int)s_w;
-    const uint32_t hA = s_hA;
-    const bool case2 = hA > (uint32_t)tr::max_alpha;
-    const uint64_t dmask = s_dmask;
+            const uint8_t* img = smem + (size_t)sl * region + (uint32_t)(si.off & 15);
+            const int w = (int)si.w;
+            const uint32_t hA = si.hA;
+            const bool case2 = hA > (uint32_t)tr::max_alpha;
+            const uint64_t dmask = si.dmask;
+            const B z1 = si.z1;
 
     // ---- planes -> lanes: thread t gathers byte t of every row (dense: verbatim;
     //      sparse: bitmap bit t, payload byte at warp prefix + ballot rank), one 8x8
     //      transpose per 8 planes, then a byte transpose assembles the lanes ----
-    const uint8_t* img = s_stage + a;
     uint64_t yb[W / 8];
 #pragma unroll
     for (int sb = 0; sb < W / 8; ++sb) yb[sb] = 0;
@@ -418,8 +441,8 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
 #pragma unroll
     for (int sb = 0; sb < W / 8; ++sb) {
         if (sb >= nblk) break;
-        const uint4 o03 = *reinterpret_cast<const uint4*>(&s_rowoff[8 * sb]);
-        const uint4 o47 = *reinterpret_cast<const uint4*>(&s_rowoff[8 * sb + 4]);
+        const uint4 o03 = *reinterpret_cast<const uint4*>(&si.rowoff[8 * sb]);
+        const uint4 o47 = *reinterpret_cast<const uint4*>(&si.rowoff[8 * sb + 4]);
         const uint32_t ro[8] = {o03.x, o03.y, o03.z, o03.w, o47.x, o47.y, o47.z, o47.w};
         const int kmax = w - 8 * sb;
         const uint32_t valid = kmax >= 8 ? 0xffu : ((1u << kmax) - 1u);
@@ -429,7 +452,7 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
 #pragma unroll
             for (int k = 0; k < 8; ++k) xb[k] = active ? img[ro[k] + tid] : 0u;
         } else {
-            const uint4 wp = *reinterpret_cast<const uint4*>(&s_wpre[warp * 64 + 8 * sb]);
+            const uint4 wp = *reinterpret_cast<const uint4*>(&si.wpre[warp * 64 + 8 * sb]);
             const uint32_t wpre[8] = {wp.x & 0xffffu, wp.x >> 16, wp.y & 0xffffu, wp.y >> 16,
                                       wp.z & 0xffffu, wp.z >> 16, wp.w & 0xffffu, wp.w >> 16};
 #pragma unroll
@@ -498,11 +521,11 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
         const B t = __shfl_up_sync(0xffffffffu, incl, k);
         if (lane >= k) incl += t;
     }
-    if (lane == 31) s_wtot[warp] = incl;
+    if (lane == 31) si.wtot[warp] = incl;
     consumer_sync<NT>();
-    B before = s_z1;
+    B before = z1;
 #pragma unroll
-    for (int q = 0; q < nwarps; ++q) before += q < warp ? s_wtot[q] : (B)0;
+    for (int q = 0; q < nwarps; ++q) before += q < warp ? si.wtot[q] : (B)0;
     before += incl - tsum;  // exclusive prefix of this thread
     const T scale = pow10_of(T{}, case2 ? 0 : (int)hA);
     const T rscale = div_rn(T(1), scale);
@@ -519,12 +542,10 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
         for (int j = 0; j < 8; ++j)
             if (i0 + j < count) dst[i0 + j] = to_value((B)(before + d[j]));
     }
-    if (tid == 0 && count > 0) dst[0] = to_value(s_z1);
-
-            } while (0);
+    if (tid == 0 && count > 0) dst[0] = to_value(z1);
         }
-        consumer_sync<NT>();
-        if (tid == 0) mbar_arrive(&s_empty[sl]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[sl]);
     }
 }
 
