@@ -134,12 +134,16 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    return done != 0;
+}
+// spin with a short sleep between failed probes: waiting warps give their issue slots
+// to the working ones
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-                     : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-    }
+    while (!mbar_try(bar, parity)) __nanosleep(32);
 }
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
@@ -152,7 +156,8 @@ __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 
-constexpr int kDecodeSlots = 3;
+constexpr int kDecodeSlots = 4;   // smem ring depth
+constexpr int kProducers = 2;     // producer warps (slots alternate between them)
 enum : uint32_t { SLOT_CHUNK = 0, SLOT_SKIP = 1, SLOT_EXIT = 2 };
 
 template <typename T>
@@ -291,7 +296,7 @@ __device__ __forceinline__ void parse_chunk(const uint8_t* p, const uint8_t* hp,
 // store.  Staging and parsing of chunk i+1, i+2 overlap the decode of chunk i; the next
 // ticket's offsets are fetched while the current copy is in flight.
 template <typename T, int NT>
-__global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* __restrict__ arc, uint64_t len,
+__global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(const uint8_t* __restrict__ arc, uint64_t len,
                                                                 geometry g, T* __restrict__ out,
                                                                 decode_ws ws) {
     using tr = lane_traits<T>;
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kDecodeSlots; ++i) {
-            mbar_init(&s_full[i], 32);       // every producer lane
+            mbar_init(&s_full[i], 32);       // every lane of the slot's producer warp
             mbar_init(&s_empty[i], nwarps);  // one per consumer warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -324,8 +329,9 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
     __syncthreads();
 
     if ((int)threadIdx.x >= NT) {
-        // ===================== producer warp =====================
+        // ===================== producer warps =====================
         const int lane = threadIdx.x & 31;
+        const uint32_t pw = (threadIdx.x - NT) >> 5;  // producer pw fills iterations pw, pw + kProducers, ...
         const bool aligned = ((uintptr_t)arc & 15) == 0;
         // next ticket: chunk index, kind, archive offset and size (lane 0 fetches)
         auto fetch = [&](uint32_t& t, uint32_t& kind, uint64_t& off, uint32_t& size) {
@@ -358,7 +364,7 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
         uint32_t t, kind, size;
         uint64_t off;
         fetch(t, kind, off, size);
-        for (uint32_t it = 0;; ++it) {
+        for (uint32_t it = pw;; it += kProducers) {
             const int sl = (int)(it % kDecodeSlots);
             if (it >= (uint32_t)kDecodeSlots) mbar_wait(&s_empty[sl], ((it / kDecodeSlots) & 1) ^ 1);
             SI& si = s_info[sl];
@@ -407,12 +413,22 @@ __global__ void __launch_bounds__(NT + 32) decode_chunks_kernel(const uint8_t* _
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool active = tid < NC;
     const uint32_t lt_mask = (1u << lane) - 1u;
+    // a producer that ran out of tickets publishes one EXIT slot and stops; the other may
+    // still hold a chunk for a later iteration, so consumers skip only the exited
+    // producer's iterations and leave once every producer has exited
+    uint32_t exited = 0;
     for (uint32_t it = 0;; ++it) {
+        const uint32_t pw = it % kProducers;
+        if ((exited >> pw) & 1u) continue;
         const int sl = (int)(it % kDecodeSlots);
         mbar_wait(&s_full[sl], (it / kDecodeSlots) & 1);
         SI& si = s_info[sl];
         const uint32_t kind = si.kind;
-        if (kind == SLOT_EXIT) break;
+        if (kind == SLOT_EXIT) {
+            exited |= 1u << pw;
+            if (exited == (1u << kProducers) - 1u) break;
+            continue;
+        }
         const uint32_t code = kind == SLOT_CHUNK ? si.code : 0u;
         if (kind == SLOT_CHUNK && code != 0u) {
             if (tid == 0) record_error(ws.error, si.chunk, code);
@@ -582,7 +598,7 @@ cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
     // persistent grid: every block co-resident (block 0 walks frames, the rest spin on it)
     int per_sm = 0, dev = 0, sms = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)threads + 32, smem))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)threads + 32 * kProducers, smem))) return e;
     if ((e = cudaGetDevice(&dev))) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev))) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
@@ -590,7 +606,7 @@ cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry
     if (grid > g.n_chunks + 1) grid = g.n_chunks + 1;
     if (grid < 2) grid = 2;
     if (ev0 && (e = cudaEventRecord(ev0, st))) return e;
-    kern<<<(unsigned)grid, threads + 32, smem, st>>>(d_archive, len, g, d_out, ws);
+    kern<<<(unsigned)grid, threads + 32 * kProducers, smem, st>>>(d_archive, len, g, d_out, ws);
     if ((e = cudaGetLastError())) return e;
     return ev1 ? cudaEventRecord(ev1, st) : cudaSuccess;
 }
