@@ -184,6 +184,12 @@ falcon_status falcon_selftest_dp(falcon_ctx* ctx, int precision, const void* d_v
                                  int candidate_alpha, int8_t* d_full, int8_t* d_literal,
                                  int8_t* d_cert, int64_t* d_g, void* stream);
 
+/* d_out[i] (double or float per precision) = the decoder's division-free inverse scale
+ * RN((T)d_g[i] / 10^alpha) (numeric.hpp:159-162), for alpha <= 21 (f64) / 9 (f32).
+ * Checked against IEEE division by tests/test_gpu_dpds.py. */
+falcon_status falcon_selftest_div(falcon_ctx* ctx, int precision, const int64_t* d_g, uint64_t n,
+                                  int alpha, void* d_out, void* stream);
+
 /* ---- synthetic inputs (synthetic.hpp:14-32 kinds; kind 5 = the pinned cfg3 kind) ---- */
 #define FALCON_KIND_WALK 0
 #define FALCON_KIND_DECIMAL 1

@@ -28,17 +28,22 @@ def _mtime(p: str) -> float:
     return os.path.getmtime(p) if os.path.exists(p) else 0.0
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines: tuple = (), out: str | None = None) -> str:
+    """Build the library; `defines` + `out` make a variant (own object dir, own .so) for
+    A/B kernel experiments."""
+    build_dir = BUILD if not defines else os.path.join(ROOT, "build", "variant_" + "_".join(d.replace("=", "") for d in defines))
+    lib = out or LIB
+    flags = FLAGS + [f"-D{d}" for d in defines]
+    os.makedirs(build_dir, exist_ok=True)
     dep = max([_mtime(os.path.join(CSRC, h)) for h in HEADERS] +
               [_mtime(os.path.join(ROOT, "include", "falcon_b200.h")), _mtime(__file__)])
     objs, jobs = [], []
     for u in UNITS:
         src = os.path.join(CSRC, u)
-        obj = os.path.join(BUILD, u.replace(".cu", ".o"))
+        obj = os.path.join(build_dir, u.replace(".cu", ".o"))
         objs.append(obj)
         if force or _mtime(obj) < max(_mtime(src), dep):
-            jobs.append([NVCC, *FLAGS, "-c", src, "-o", obj] + (["-Xptxas", "-v"] if verbose else []))
+            jobs.append([NVCC, *flags, "-c", src, "-o", obj] + (["-Xptxas", "-v"] if verbose else []))
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -50,10 +55,10 @@ def build(verbose: bool = False, force: bool = False) -> str:
         for out in ex.map(run, jobs):
             if verbose and out:
                 print(out)
-    if force or jobs or _mtime(LIB) < max(_mtime(o) for o in objs):
+    if force or jobs or _mtime(lib) < max(_mtime(o) for o in objs):
         run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
-             "-o", LIB, *objs, "-lpthread"])
-    return LIB
+             "-o", lib, *objs, "-lpthread"])
+    return lib
 
 
 if __name__ == "__main__":

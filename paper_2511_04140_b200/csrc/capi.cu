@@ -332,6 +332,17 @@ falcon_status falcon_selftest_dp(falcon_ctx* ctx, int precision, const void* d_v
     return FALCON_OK;
 }
 
+falcon_status falcon_selftest_div(falcon_ctx* ctx, int precision, const int64_t* d_g, uint64_t n, int alpha,
+                                  void* d_out, void* stream) {
+    if (!ctx) return set_error(FALCON_ERR_INVALID, "null context");
+    if (alpha < 0 || alpha > (precision == 0 ? 21 : 9)) return set_error(FALCON_ERR_INVALID, "alpha out of range");
+    device_guard dg(ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    FB_CUDA(launch_selftest_div(precision, d_g, n, alpha, d_out, st));
+    FB_CUDA(cudaStreamSynchronize(st));
+    return FALCON_OK;
+}
+
 // ---- per-chunk operators ---------------------------------------------------------
 falcon_status falcon_compress_chunk(falcon_ctx* ctx, int precision, const void* values,
                                     uint32_t chunk_n, uint8_t* out, uint64_t out_cap,

@@ -102,10 +102,10 @@ __device__ void walk_frames(const uint8_t* __restrict__ arc, uint64_t len, const
 
 }  // namespace
 
-// RN(g / p) for the Case-1 inverse scale (numeric.hpp:159-162): one Markstein
-// correction step from the rounded reciprocal, accepted only when the exact residual
-// test of dpds.cuh (2) proves it is the correctly rounded quotient; otherwise IEEE
-// division.  f32 keeps the IEEE division.
+// RN(g / p) for the Case-1 inverse scale (numeric.hpp:159-162) at alpha = 22 (beyond
+// the division-free range of dpds.cuh): one Markstein correction step from the rounded
+// reciprocal, accepted only when the exact residual test of dpds.cuh (2) proves it is
+// the correctly rounded quotient; otherwise IEEE division.  f32 (alpha 10) divides.
 __device__ __noinline__ double ddiv_fallback(double a, double b) { return __ddiv_rn(a, b); }
 
 __device__ __forceinline__ double inverse_scale_rn(double gd, double p, double rp) {
@@ -140,10 +140,21 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
                  : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
     return done != 0;
 }
-// spin with a short sleep between failed probes: waiting warps give their issue slots
-// to the working ones
+// blocking wait: try_wait with a suspend-time hint parks the warp in hardware until the
+// phase completes (or the hint expires), so waiting warps take no issue slots
+__device__ __forceinline__ bool mbar_try_suspend(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done) : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u) : "memory");
+    return done != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef FB_AB_SPIN
     while (!mbar_try(bar, parity)) __nanosleep(32);
+#else
+    while (!mbar_try_suspend(bar, parity)) {
+    }
+#endif
 }
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
@@ -160,23 +171,31 @@ constexpr int kDecodeSlots = 4;   // smem ring depth
 constexpr int kProducers = 2;     // producer warps (slots alternate between them)
 enum : uint32_t { SLOT_CHUNK = 0, SLOT_SKIP = 1, SLOT_EXIT = 2 };
 
+// value staging for coalesced stores: [8][NT + 2] values (+ value 0), reusing the slot
+__host__ __device__ __forceinline__ uint32_t decode_stage_stride(uint32_t nt) { return nt + 2; }
+
 template <typename T>
 __host__ __device__ __forceinline__ uint32_t decode_region_bytes(uint32_t chunk_n) {
     using tr = lane_traits<T>;
     const uint32_t nc = (chunk_n - 1) / 8;
-    return (uint32_t)(tr::header + (tr::width + 7) / 8 + tr::width * nc + 16 + 15) & ~15u;
+    const uint32_t nt = nc <= 256 ? (nc < 32 ? 32 : (nc + 31) / 32 * 32) : (nc <= 512 ? 512 : 1024);
+    const uint32_t raw = (uint32_t)(tr::header + (tr::width + 7) / 8 + tr::width * nc + 16 + 15) & ~15u;
+    const uint32_t vals = (uint32_t)((8 * decode_stage_stride(nt) + 1) * sizeof(T) + 15) & ~15u;
+    return raw > vals ? raw : vals;
 }
 
 // Everything the consumers need about one staged chunk, written by the producer warp.
-template <typename B, int NW>
+template <typename T, typename B, int NW>
 struct __align__(16) slot_info {
     uint32_t rowoff[64];      // plane p: row offset from the chunk's first byte
     uint16_t wpre[NW * 64];   // [warp][plane]: sparse payload bytes of the warps before
     uint64_t dmask;           // bit p: plane p is dense
     uint64_t off;             // archive offset of the chunk
+    uint64_t v0;              // index of the chunk's first value
+    T scale, rscale;          // 10^alpha and RN(1 / 10^alpha)
     B z1;
     B wtot[NW];               // consumer scan scratch
-    uint32_t chunk, size, kind, code, w, hA;
+    uint32_t chunk, size, kind, code, w, hA, count;
 };
 
 // Parse + validate one staged chunk in the reference's order (chunk_codec.hpp:92-117,
@@ -236,8 +255,6 @@ __device__ __forceinline__ void parse_chunk(const uint8_t* p, const uint8_t* hp,
             int bad = 64;                 // first row failing a truncation check
             uint32_t bad_code = 0;
             uint64_t sparse = ((uint64_t)sm1 << 32) | sm0;
-            // lane q < NW counts bitmap bytes [4q, 4q + 4) (consumer warp q's columns)
-            const uint32_t g0 = 4u * (uint32_t)lane;
             while (sparse) {
                 const int r = __ffsll((long long)sparse) - 1;
                 sparse &= sparse - 1;
@@ -245,20 +262,35 @@ __device__ __forceinline__ void parse_chunk(const uint8_t* p, const uint8_t* hp,
                                            : __popc(dm0) + __popc(dm1 & ((1u << (r - 32)) - 1u));
                 const uint32_t rp = pos0 + nd * (uint32_t)NC + acc;
                 if (size < rp + (uint32_t)BM) { bad = r; bad_code = DEV_E_BITMAP_TRUNC; break; }
-                uint32_t pc = 0;
-                if (lane < NW) {
+                // chain: one bitmap byte per lane, popcounts summed by REDUX (the next
+                // sparse row's offset needs only the total)
+                const uint32_t pa = lane < BM ? __popc(p[rp + lane]) : 0u;
+                const uint32_t pb = lane + 32 < BM ? __popc(p[rp + lane + 32]) : 0u;
+                const uint32_t tot = __reduce_add_sync(0xffffffffu, pa + pb);
+                // off the chain: consumer warp q's payload prefix = popcounts of bitmap
+                // bytes [0, 4q) (exclusive scan of 4-byte group sums over lanes q < NW)
+                {
+                    uint32_t gs = pa;   // group q = lanes 4q..4q+3 of the byte counts
+                    gs += __shfl_down_sync(0xffffffffu, gs, 1);
+                    gs += __shfl_down_sync(0xffffffffu, gs, 2);
+                    if (NW > 8) {       // groups 8..15 live in the second half (bytes 32..63)
+                        uint32_t gh = pb;
+                        gh += __shfl_down_sync(0xffffffffu, gh, 1);
+                        gh += __shfl_down_sync(0xffffffffu, gh, 2);
+                        const uint32_t hsrc = __shfl_sync(0xffffffffu, gh, (4 * lane - 32) & 31);
+                        gs = __shfl_sync(0xffffffffu, gs, (4 * lane) & 31);
+                        gs = lane >= 8 ? hsrc : gs;
+                    } else {
+                        gs = __shfl_sync(0xffffffffu, gs, (4 * lane) & 31);
+                    }
+                    uint32_t incl = gs;
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (g0 + k < (uint32_t)BM) pc += __popc(p[rp + g0 + k]);
+                    for (int d = 1; d < NW; d <<= 1) {
+                        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+                        if (lane >= d) incl += t;
+                    }
+                    if (lane < NW) si.wpre[lane * 64 + (w - 1 - r)] = (uint16_t)(incl - gs);
                 }
-                uint32_t incl = pc;  // inclusive scan over the (<= 16) groups
-#pragma unroll
-                for (int d = 1; d < NW; d <<= 1) {
-                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
-                    if (lane >= d) incl += t;
-                }
-                const uint32_t tot = __shfl_sync(0xffffffffu, incl, NW - 1);
-                if (lane < NW) si.wpre[lane * 64 + (w - 1 - r)] = (uint16_t)(incl - pc);
                 if (size - rp - (uint32_t)BM < tot) { bad = r; bad_code = DEV_E_PAYLOAD_TRUNC; break; }
                 if (r0 > r) acc0 += (uint32_t)BM + tot;
                 if (r1 > r) acc1 += (uint32_t)BM + tot;
@@ -289,12 +321,12 @@ __device__ __forceinline__ void parse_chunk(const uint8_t* p, const uint8_t* hp,
 }
 
 // Persistent, warp-specialized decode.  Block 0 is the frame walker.  In every other
-// block the last warp is the producer: it takes chunk tickets, waits for the walker to
-// publish the chunk's batch, streams the chunk bytes (16-B cp.async at the source's
-// 16-B phase) into a ring of kDecodeSlots smem slots, parses and validates the staged
-// chunk, and hands the slot to the NT consumer threads, which only gather, scan and
-// store.  Staging and parsing of chunk i+1, i+2 overlap the decode of chunk i; the next
-// ticket's offsets are fetched while the current copy is in flight.
+// block the last kProducers warps are producers: each takes chunk tickets, waits for
+// the walker to publish its chunk's batch, streams the chunk bytes (16-B
+// cp.async at the source's 16-B phase) into a ring of kDecodeSlots smem slots, parses
+// and validates the staged chunk, and hands the slot to the NT consumer threads, which
+// only gather, scan and store.  Staging and parsing of later chunks overlap the decode
+// of the current one; the next chunk's offsets are fetched while a copy is in flight.
 template <typename T, int NT>
 __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(const uint8_t* __restrict__ arc, uint64_t len,
                                                                 geometry g, T* __restrict__ out,
@@ -304,7 +336,7 @@ __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(con
     using S = typename tr::S;
     constexpr int W = tr::width;
     constexpr int nwarps = NT / 32;
-    using SI = slot_info<B, nwarps>;
+    using SI = slot_info<T, B, nwarps>;
 
     if (blockIdx.x == 0) {
         walk_frames(arc, len, g, ws);
@@ -333,17 +365,18 @@ __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(con
         const int lane = threadIdx.x & 31;
         const uint32_t pw = (threadIdx.x - NT) >> 5;  // producer pw fills iterations pw, pw + kProducers, ...
         const bool aligned = ((uintptr_t)arc & 15) == 0;
-        // next ticket: chunk index, kind, archive offset and size (lane 0 fetches)
-        auto fetch = [&](uint32_t& t, uint32_t& kind, uint64_t& off, uint32_t& size) {
-            t = 0;
-            kind = SLOT_CHUNK;
+        // dynamic chunk tickets (measured better balanced than static striding); lane 0
+        // waits for the chunk's batch frame and loads its offset and size
+        auto fetch = [&](uint32_t it, uint32_t& t, uint32_t& kind, uint64_t& off, uint32_t& size) {
+            uint32_t tk = 0;
+            if (lane == 0) tk = atomicAdd(ws.ticket, 1u);
+            const uint64_t c = __shfl_sync(0xffffffffu, tk, 0);
+            (void)it;
+            t = (uint32_t)c;
+            kind = c < g.n_chunks ? SLOT_CHUNK : SLOT_EXIT;
             off = 0;
             size = 0;
-            if (lane == 0) t = atomicAdd(ws.ticket, 1u);
-            t = __shfl_sync(0xffffffffu, t, 0);
-            if (t >= g.n_chunks) {
-                kind = SLOT_EXIT;
-            } else if (lane == 0) {
+            if (kind == SLOT_CHUNK && lane == 0) {
                 const uint32_t b = t / g.cpb;
                 while (ld_acquire32(&ws.ready[b]) == 0) {
                     if (*(volatile unsigned long long*)ws.abort_at <= b) {
@@ -363,7 +396,7 @@ __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(con
         };
         uint32_t t, kind, size;
         uint64_t off;
-        fetch(t, kind, off, size);
+        fetch(pw, t, kind, off, size);
         for (uint32_t it = pw;; it += kProducers) {
             const int sl = (int)(it % kDecodeSlots);
             if (it >= (uint32_t)kDecodeSlots) mbar_wait(&s_empty[sl], ((it / kDecodeSlots) & 1) ^ 1);
@@ -385,10 +418,10 @@ __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(con
                     }
                 }
             }
-            // the next ticket's offsets load while the copy is in flight
+            // the next chunk's offsets load while the copy is in flight
             uint32_t t2 = 0, kind2 = SLOT_EXIT, size2 = 0;
             uint64_t off2 = 0;
-            if (kind != SLOT_EXIT) fetch(t2, kind2, off2, size2);
+            if (kind != SLOT_EXIT) fetch(it + kProducers, t2, kind2, off2, size2);
             asm volatile("cp.async.wait_all;" ::: "memory");
             __syncwarp();
             if (kind == SLOT_CHUNK) parse_chunk<T, nwarps>(buf + a, staged ? buf + a : arc + off, size, !staged, NC, BM, si, lane);
@@ -397,6 +430,17 @@ __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(con
                 si.chunk = t;
                 si.off = off;
                 si.size = size;
+                if (kind == SLOT_CHUNK) {
+                    // chunk-uniform values the consumers would otherwise each recompute
+                    const uint32_t b = t / g.cpb;
+                    const uint32_t ci = t - b * g.cpb;
+                    const uint64_t left = g.values_in(b) - (uint64_t)ci * n;
+                    si.v0 = (uint64_t)b * g.batch_values + (uint64_t)ci * n;
+                    si.count = left < n ? (uint32_t)left : n;
+                    const T sc = pow10_of(T{}, si.hA > (uint32_t)tr::max_alpha ? 0 : (int)si.hA);
+                    si.scale = sc;
+                    si.rscale = div_rn(T(1), sc);
+                }
             }
             __syncwarp();
             mbar_arrive(&s_full[sl]);
@@ -413,7 +457,7 @@ __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(con
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool active = tid < NC;
     const uint32_t lt_mask = (1u << lane) - 1u;
-    // a producer that ran out of tickets publishes one EXIT slot and stops; the other may
+    // a producer that ran out of chunks publishes one EXIT slot and stops; the other may
     // still hold a chunk for a later iteration, so consumers skip only the exited
     // producer's iterations and leave once every producer has exited
     uint32_t exited = 0;
@@ -433,13 +477,8 @@ __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(con
         if (kind == SLOT_CHUNK && code != 0u) {
             if (tid == 0) record_error(ws.error, si.chunk, code);
         } else if (kind == SLOT_CHUNK) {
-            const uint32_t c = si.chunk;
-            const uint32_t b = c / g.cpb;
-            const uint32_t ci = c - b * g.cpb;
-            const uint64_t bcount = g.values_in(b);
-            const uint64_t v0 = (uint64_t)b * g.batch_values + (uint64_t)ci * n;
-            const uint64_t left = bcount - (uint64_t)ci * n;
-            const uint32_t count = left < n ? (uint32_t)left : n;
+            const uint64_t v0 = si.v0;
+            const uint32_t count = si.count;
             const uint8_t* img = smem + (size_t)sl * region + (uint32_t)(si.off & 15);
             const int w = (int)si.w;
             const uint32_t hA = si.hA;
@@ -543,22 +582,51 @@ __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(con
 #pragma unroll
     for (int q = 0; q < nwarps; ++q) before += q < warp ? si.wtot[q] : (B)0;
     before += incl - tsum;  // exclusive prefix of this thread
-    const T scale = pow10_of(T{}, case2 ? 0 : (int)hA);
-    const T rscale = div_rn(T(1), scale);
-    auto to_value = [&](B gv) -> T {
-        if (case2) return value_of(unzigzag<B>(gv));
-        return inverse_scale_rn(from_i64(T{}, (long long)(S)gv), scale, rscale);  // numeric.hpp:159-162
-    };
-    // values straight from registers: thread t writes values 8t+1..8t+8 (a warp's eight
-    // stores cover 2 KB contiguously); padded lanes are dropped (transform.hpp:96)
+    const T scale = si.scale, rscale = si.rscale;
+    // Case 1 divides by 10^alpha (numeric.hpp:159-162) without a division (dpds.cuh);
+    // padded lanes are dropped (transform.hpp:96).  Values go through the slot (free once
+    // every consumer passed the scan barrier) as [j][t] (conflict-free), then out with
+    // lane-contiguous stores: a warp writes 256 consecutive bytes per instruction instead
+    // of 32 scattered 8-B pieces.
     T* dst = out + v0;
-    if (active) {
-        const uint32_t i0 = 8u * (uint32_t)tid + 1u;
+#ifdef FB_AB_DIRECT_STORE
+    const uint32_t i0 = 8u * (uint32_t)tid + 1u;
+    auto store = [&](auto to_value) {
+        if (active) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (i0 + j < count) dst[i0 + j] = to_value((B)(before + d[j]));
+            for (int j = 0; j < 8; ++j)
+                if (i0 + j < count) dst[i0 + j] = to_value((B)(before + d[j]));
+        }
+        if (tid == 0 && count > 0) dst[0] = to_value(z1);
+    };
+#else
+    T* vstage = reinterpret_cast<T*>(smem + (size_t)sl * region);
+    constexpr uint32_t SP = NT + 2;  // decode_stage_stride(NT)
+    auto store = [&](auto to_value) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) vstage[j * SP + tid] = to_value((B)(before + d[j]));
+        if (tid == 0) vstage[8 * SP] = to_value(z1);
+    };
+#endif
+#ifdef FB_AB_NO_MARKSTEIN
+    constexpr int kMark = -1;
+#else
+    constexpr int kMark = sizeof(T) == 8 ? kMarksteinMaxAlpha64 : kMarksteinMaxAlpha32;
+#endif
+    if (case2) {
+        store([&](B gv) -> T { return value_of(unzigzag<B>(gv)); });
+    } else if ((int)hA <= kMark) {
+        store([&](B gv) -> T { return div_pow10_markstein(from_i64(T{}, (long long)(S)gv), scale, rscale); });
+    } else {
+        store([&](B gv) -> T { return inverse_scale_rn(from_i64(T{}, (long long)(S)gv), scale, rscale); });
     }
-    if (tid == 0 && count > 0) dst[0] = to_value(z1);
+#ifndef FB_AB_DIRECT_STORE
+    consumer_sync<NT>();
+    for (uint32_t i = tid; i < count; i += NT) {
+        const uint32_t k = i - 1u;  // value i >= 1 is lane k: thread k / 8, register k % 8
+        dst[i] = i == 0 ? vstage[8 * SP] : vstage[(k & 7u) * SP + (k >> 3)];
+    }
+#endif
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sl]);

@@ -162,6 +162,28 @@ __device__ __forceinline__ int dp_alpha_k(T v) {
 template <typename T>
 __device__ __noinline__ int dp_alpha_full(T v) { return dp_alpha_k<T, 1>(v); }
 
+// ---- inverse scale without a division (decode hot loop) ----
+// RN(g / 10^a) (numeric.hpp:159-162) from the correctly rounded reciprocal rp = RN(1/p):
+//   q0 = RN(g * rp);  r = g - q0 * p (exact, one FMA);  q = RN(q0 + r * rp)
+// is exactly RN(g/p) when 5^a < 2^(P-2) (P = 53 / 24: a <= 21 f64, a <= 9 f32).  Proof
+// (DESIGN.md 4): |q0 - x| < 2 ulp(x) for x = g/p, so q0 + r*rp = x + (x - q0) * d with
+// |d| = |p*rp - 1| <= 2^-P, an error below 2^(E-2P+2) in x's binade E.  A midpoint m of
+// that binade is an odd multiple of 2^(E-P) and g - m*p is a multiple of 2^(E-P+a) that is
+// never zero (m*p has an odd part of more than P bits, g is a P-bit float), so
+// |x - m| >= 2^(E-P) / 5^a > 2^(E-2P+2): no midpoint separates x from q0 + r*rp.
+constexpr int kMarksteinMaxAlpha64 = 21;
+constexpr int kMarksteinMaxAlpha32 = 9;
+__device__ __forceinline__ double div_pow10_markstein(double g, double p, double rp) {
+    const double q0 = __dmul_rn(g, rp);
+    const double r = __fma_rn(-q0, p, g);
+    return __fma_rn(r, rp, q0);
+}
+__device__ __forceinline__ float div_pow10_markstein(float g, float p, float rp) {
+    const float q0 = __fmul_rn(g, rp);
+    const float r = __fmaf_rn(-q0, p, g);
+    return __fmaf_rn(r, rp, q0);
+}
+
 enum : int { CERT_UNDECIDED = 0, CERT_OK = 1, CERT_EXC = 2 };
 
 // Branch-free form of dp_certify for the encoder's hot loop: same verdicts (the

@@ -34,7 +34,7 @@ encode_ws carve_encode_ws(void* scratch, const geometry& g, uint32_t* ticket,
 
 // Scratch for one decompress launch.
 struct decode_ws {
-    uint32_t* ticket;             // ticket 0 = frame walker, ticket c+1 = chunk c
+    uint32_t* ticket;             // chunk ticket counter
     uint32_t* ready;              // [n_batches] batch frame located (1) or not (0)
     unsigned long long* abort_at; // first batch the walker could not locate (~0 = none)
     uint64_t* chunk_off;          // [n_chunks] archive offset of each chunk
@@ -60,6 +60,8 @@ cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry
 
 cudaError_t launch_selftest_dp(int prec, const void* v, uint64_t n, int A, int8_t* full,
                                int8_t* lit, int8_t* cert, int64_t* g, cudaStream_t st);
+
+cudaError_t launch_selftest_div(int prec, const int64_t* g, uint64_t n, int alpha, void* out, cudaStream_t st);
 
 // One-time upload of the pow10 / decade tables (numeric.hpp:17-41, numeric.cpp:10-39).
 cudaError_t upload_tables();

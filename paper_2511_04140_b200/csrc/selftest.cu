@@ -38,6 +38,26 @@ __global__ void selftest_dp_kernel(const T* __restrict__ v, uint64_t n, int A, i
     }
 }
 
+// out[i] = the decoder's division-free inverse scale of g[i] at scale alpha
+template <typename T>
+__global__ void selftest_div_kernel(const int64_t* __restrict__ g, uint64_t n, int alpha, T* __restrict__ out) {
+    const T p = fpx<T>::pow10(alpha);
+    const T rp = div_rn(T(1), p);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const T gd = sizeof(T) == 8 ? (T)__ll2double_rn(g[i]) : (T)__ll2float_rn(g[i]);
+        out[i] = div_pow10_markstein(gd, p, rp);
+    }
+}
+
+cudaError_t launch_selftest_div(int prec, const int64_t* g, uint64_t n, int alpha, void* out, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((n + 255) / 256 < 148 * 32 ? (n + 255) / 256 : 148 * 32);
+    if (prec == 0) selftest_div_kernel<double><<<blocks, 256, 0, st>>>(g, n, alpha, static_cast<double*>(out));
+    else selftest_div_kernel<float><<<blocks, 256, 0, st>>>(g, n, alpha, static_cast<float*>(out));
+    return cudaGetLastError();
+}
+
 cudaError_t launch_selftest_dp(int prec, const void* v, uint64_t n, int A, int8_t* f, int8_t* l,
                                int8_t* c, int64_t* g, cudaStream_t st) {
     const unsigned blocks = (unsigned)((n + 255) / 256 < 148 * 32 ? (n + 255) / 256 : 148 * 32);

@@ -28,7 +28,7 @@ EXPORTED = [
     "falcon_compress_device_async", "falcon_decompress_device", "falcon_decompress_device_async",
     "falcon_ctx_sync", "falcon_compress_stream", "falcon_decompress_stream", "falcon_compress_host",
     "falcon_decompress_host", "falcon_compress_chunk", "falcon_decompress_chunk", "falcon_synth_fill",
-    "falcon_ctx_set_kernel_events", "falcon_selftest_dp",
+    "falcon_ctx_set_kernel_events", "falcon_selftest_dp", "falcon_selftest_div",
 ]
 
 
@@ -83,9 +83,12 @@ def load() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB):
-        raise ImportError(f"{LIB} is missing: run __graft_entry__.build() (no CPU fallback exists)")
-    L = C.CDLL(LIB)
+    # FALCON_B200_LIB selects an alternative in-tree build (A/B kernel experiments,
+    # scripts/ab.sh); the default is the package's own library
+    path = os.environ.get("FALCON_B200_LIB", LIB)
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+    L = C.CDLL(path)
     vp, u64, u32, i32 = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int
     L.falcon_last_error.restype = C.c_char_p
     L.falcon_ctx_create.argtypes = [i32, C.POINTER(vp)]
@@ -103,6 +106,7 @@ def load() -> C.CDLL:
     L.falcon_ctx_sync.argtypes = [vp, vp]
     L.falcon_ctx_set_kernel_events.argtypes = [vp, vp, vp, vp, vp]
     L.falcon_selftest_dp.argtypes = [vp, i32, vp, u64, i32, vp, vp, vp, vp, vp]
+    L.falcon_selftest_div.argtypes = [vp, i32, vp, u64, i32, vp, vp]
     L.falcon_compress_stream.argtypes = [vp, i32, READ_FN, vp, STORE_FN, vp,
                                          C.POINTER(PipelineOptions), C.POINTER(PipelineStats)]
     L.falcon_decompress_stream.argtypes = [vp, i32, vp, u64, PUT_FN, vp, C.POINTER(PipelineOptions),
@@ -263,6 +267,15 @@ class Codec:
                                            candidate_alpha, C.c_void_p(f.data_ptr()), C.c_void_p(lit.data_ptr()),
                                            C.c_void_p(c.data_ptr()), C.c_void_p(g.data_ptr()), st))
         return f.cpu().numpy(), lit.cpu().numpy(), c.cpu().numpy(), g.cpu().numpy()
+
+    def selftest_div(self, g, alpha: int, precision: int):
+        """g: int64 CUDA tensor.  Returns the decoder's inverse scale of g at alpha (numpy)."""
+        import torch
+        out = torch.empty(g.numel(), dtype=torch.float64 if precision == 0 else torch.float32, device=g.device)
+        st = C.c_void_p(torch.cuda.current_stream(g.device).cuda_stream)
+        _check(self.lib.falcon_selftest_div(self.ctx, precision, C.c_void_p(g.data_ptr()), g.numel(), alpha,
+                                            C.c_void_p(out.data_ptr()), st))
+        return out.cpu().numpy()
 
     def sync(self, stream=None):
         import torch

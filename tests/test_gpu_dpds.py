@@ -108,3 +108,30 @@ def test_certification_rate_on_clean_decimals(codec):
     _, _, cert, _ = codec.selftest_dp(torch.from_numpy(v).cuda(), 2)
     assert ((cert & 3) == 1).mean() > 0.999
     assert ((cert & 4) != 0).mean() > 0.999   # the encoder's lean form decides them too
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_division_free_inverse_scale_is_correctly_rounded(codec, prec):
+    """The decoder's Markstein inverse scale (dpds.cuh) equals IEEE g / 10^alpha for every
+    alpha it is used at (numeric.hpp:159-162: (T)g / pow10<T>(alpha))."""
+    rng = np.random.default_rng(77 + prec)
+    top = 63 if prec == 0 else 31
+    parts = [rng.integers(-(1 << 53), 1 << 53, 600_000, dtype=np.int64),
+             rng.integers(-(1 << 20), 1 << 20, 300_000, dtype=np.int64),
+             rng.integers(-(1 << (top - 1)), 1 << (top - 1), 300_000, dtype=np.int64),
+             np.arange(-5000, 5000, dtype=np.int64)]
+    g = np.concatenate(parts)
+    if prec == 1:
+        g = g.astype(np.int32).astype(np.int64)   # f32 lanes carry int32 integers
+    d = torch.from_numpy(g).cuda()
+    for alpha in range(0, 22 if prec == 0 else 10):
+        got = codec.selftest_div(d, alpha, prec)
+        if prec == 0:
+            want = g.astype(np.float64) / np.float64(10.0 ** alpha)
+            assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), f"alpha={alpha}"
+        else:
+            p = np.float32(1)
+            for _ in range(alpha):
+                p = np.float32(p * np.float32(10))
+            want = g.astype(np.float32) / p
+            assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), f"alpha={alpha}"
