@@ -167,8 +167,15 @@ __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 
-constexpr int kDecodeSlots = 4;   // smem ring depth
-constexpr int kProducers = 2;     // producer warps (slots alternate between them)
+#ifndef FB_DECODE_PRODUCERS
+#define FB_DECODE_PRODUCERS 2
+#endif
+#ifndef FB_DECODE_SLOTS
+#define FB_DECODE_SLOTS 4
+#endif
+constexpr int kDecodeSlots = FB_DECODE_SLOTS;   // smem ring depth (a multiple of kProducers:
+constexpr int kProducers = FB_DECODE_PRODUCERS; // each slot is refilled by one producer only)
+static_assert(kDecodeSlots % kProducers == 0, "slot reuse must stay within one producer");
 enum : uint32_t { SLOT_CHUNK = 0, SLOT_SKIP = 1, SLOT_EXIT = 2 };
 
 // value staging for coalesced stores: [8][NT + 2] values (+ value 0), reusing the slot
@@ -262,6 +269,23 @@ __device__ __forceinline__ void parse_chunk(const uint8_t* p, const uint8_t* hp,
                                            : __popc(dm0) + __popc(dm1 & ((1u << (r - 32)) - 1u));
                 const uint32_t rp = pos0 + nd * (uint32_t)NC + acc;
                 if (size < rp + (uint32_t)BM) { bad = r; bad_code = DEV_E_BITMAP_TRUNC; break; }
+#ifdef FB_AB_OLDPARSE
+                uint32_t pc = 0;
+                const uint32_t g0 = 4u * (uint32_t)lane;
+                if (lane < NW) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (g0 + k < (uint32_t)BM) pc += __popc(p[rp + g0 + k]);
+                }
+                uint32_t incl = pc;
+#pragma unroll
+                for (int d = 1; d < NW; d <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += t;
+                }
+                const uint32_t tot = __shfl_sync(0xffffffffu, incl, NW - 1);
+                if (lane < NW) si.wpre[lane * 64 + (w - 1 - r)] = (uint16_t)(incl - pc);
+#else
                 // chain: one bitmap byte per lane, popcounts summed by REDUX (the next
                 // sparse row's offset needs only the total)
                 const uint32_t pa = lane < BM ? __popc(p[rp + lane]) : 0u;
@@ -291,6 +315,7 @@ __device__ __forceinline__ void parse_chunk(const uint8_t* p, const uint8_t* hp,
                     }
                     if (lane < NW) si.wpre[lane * 64 + (w - 1 - r)] = (uint16_t)(incl - gs);
                 }
+#endif
                 if (size - rp - (uint32_t)BM < tot) { bad = r; bad_code = DEV_E_PAYLOAD_TRUNC; break; }
                 if (r0 > r) acc0 += (uint32_t)BM + tot;
                 if (r1 > r) acc1 += (uint32_t)BM + tot;
@@ -510,11 +535,14 @@ __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(con
             const uint4 wp = *reinterpret_cast<const uint4*>(&si.wpre[warp * 64 + 8 * sb]);
             const uint32_t wpre[8] = {wp.x & 0xffffu, wp.x >> 16, wp.y & 0xffffu, wp.y >> 16,
                                       wp.z & 0xffffu, wp.z >> 16, wp.w & 0xffffu, wp.w >> 16};
+            const uint32_t bsh = 7u - ((uint32_t)tid & 7u);
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                const bool vk = (valid >> k) & 1u, dk = (dblk >> k) & 1u;
-                const uint32_t bmb = (vk && !dk && active) ? img[ro[k] + (tid >> 3)] : 0u;
-                const uint32_t bit = (bmb >> (7 - (tid & 7))) & 1u;
+                xb[k] = 0u;
+                if (k >= kmax) continue;  // uniform: rows above w
+                const bool dk = (dblk >> k) & 1u;
+                const uint32_t bmb = (!dk && active) ? img[ro[k] + (tid >> 3)] : 0u;
+                const uint32_t bit = (bmb >> bsh) & 1u;
                 const uint32_t m = __ballot_sync(0xffffffffu, bit);
                 const uint32_t idx = dk ? ro[k] + tid : ro[k] + BM + wpre[k] + __popc(m & lt_mask);
                 xb[k] = ((dk && active) || bit) ? img[idx] : 0u;
@@ -622,9 +650,16 @@ __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(con
     }
 #ifndef FB_AB_DIRECT_STORE
     consumer_sync<NT>();
-    for (uint32_t i = tid; i < count; i += NT) {
-        const uint32_t k = i - 1u;  // value i >= 1 is lane k: thread k / 8, register k % 8
-        dst[i] = i == 0 ? vstage[8 * SP] : vstage[(k & 7u) * SP + (k >> 3)];
+    {
+        // value i = tid + NT m (m = 0..8) is lane k = i - 1: thread k / 8, register k % 8;
+        // NT is a multiple of 8, so k % 8 is fixed per thread and k / 8 steps by NT / 8
+        const int kb = tid - 1;
+        const T* vsrc = vstage + (kb & 7) * (int)SP + (kb >> 3);
+#pragma unroll
+        for (uint32_t m = 0; m < 9; ++m) {
+            const uint32_t i = (uint32_t)tid + NT * m;
+            if (m * NT < 8u * NT + 1u && i < count) dst[i] = i == 0 ? vstage[8 * SP] : vsrc[(NT / 8) * m];
+        }
     }
 #endif
         }
