@@ -28,13 +28,15 @@ __device__ __forceinline__ uint32_t ld_u32_le(const uint8_t* p) {
 }
 
 // Frame walker: validates frames in archive order and publishes per-chunk offsets.
+// Per batch the size table is read with lane-contiguous loads into smem (segments of
+// `cap` entries), scanned block-wide, and the chunk offsets/sizes are written back with
+// lane-contiguous stores, so one batch costs about one DRAM round trip plus the fence.
 __device__ void walk_frames(const uint8_t* __restrict__ arc, uint64_t len, const geometry& g,
-                            const decode_ws& ws) {
+                            const decode_ws& ws, uint4* s_raw, uint32_t* s_pref, uint32_t cap) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nthreads = blockDim.x, nwarps = nthreads >> 5;
     __shared__ uint32_t s_cnt, s_code;
-    __shared__ uint64_t s_wsum[32];
-    __shared__ uint64_t s_payload;
+    __shared__ uint32_t s_wsum[32];
     uint64_t cursor = g.header_bytes;
     for (uint64_t b = 0; b < g.n_batches; ++b) {
         const uint64_t first = b * g.cpb;
@@ -50,52 +52,96 @@ __device__ void walk_frames(const uint8_t* __restrict__ arc, uint64_t len, const
         __syncthreads();
         uint32_t code = s_code;
         const uint32_t cnt = code ? 0 : s_cnt;
-        const uint64_t table = cursor + 4;
-        // thread-contiguous ranges of the size table, block exclusive scan of their sums
-        const uint32_t per = (cnt + nthreads - 1) / nthreads;
-        const uint32_t i0 = min(cnt, (uint32_t)tid * per), i1 = min(cnt, i0 + per);
-        uint64_t mine = 0;
-        for (uint32_t i = i0; i < i1; ++i) mine += ld_u32_le(arc + table + 4 * (uint64_t)i);
-        uint64_t incl = mine;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint64_t t = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= d) incl += t;
-        }
-        if (lane == 31) s_wsum[warp] = incl;
         __syncthreads();
-        uint64_t before = 0, payload = 0;
-        for (int w = 0; w < nwarps; ++w) {
-            if (w < warp) before += s_wsum[w];
-            payload += s_wsum[w];
+        const uint64_t table = cursor + 4;
+        const uint64_t pay0 = table + 4 * (uint64_t)cnt;   // first chunk's payload
+        // the offsets are written only for a frame with the expected chunk count; the
+        // payload-truncation check (container.cpp:127-128) needs the full sum first
+        const bool write = cnt == g.chunks_in(b);
+        uint64_t carry = 0;
+        for (uint32_t seg = 0; seg < cnt; seg += cap) {
+            const uint32_t m = cnt - seg < cap ? cnt - seg : cap;
+            // the segment's table bytes: 16-B vectors (all loads in flight at once), then
+            // entries from smem.  s_raw holds the span from the vector below the table.
+            const uint64_t tb = table + 4 * (uint64_t)seg;
+            const uint64_t v0 = tb & ~15ull;
+            const uint32_t ph = (uint32_t)(tb - v0);
+            const uint32_t nvec = (ph + 4 * m + 15) >> 4;
+            const bool vec_ok = (((uintptr_t)arc) & 15) == 0;
+#pragma unroll 4
+            for (uint32_t v = tid; v < nvec; v += nthreads) {
+                const uint64_t at = v0 + 16ull * v;
+                uint4 x;
+                if (vec_ok && at + 16 <= len) {
+                    x = __ldg(reinterpret_cast<const uint4*>(arc + at));
+                } else {  // unaligned archive or its last bytes
+                    uint32_t wv[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        wv[q] = 0;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint64_t a = at + 4 * q + k;
+                            if (a < len) wv[q] |= (uint32_t)arc[a] << (8 * k);
+                        }
+                    }
+                    x = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                }
+                s_raw[v] = x;
+            }
+            __syncthreads();
+            const uint8_t* rb = reinterpret_cast<const uint8_t*>(s_raw) + ph;
+            auto entry = [&](uint32_t i) -> uint32_t { return ld_u32_le(rb + 4 * i); };
+            // thread-contiguous ranges: local sums, block exclusive scan, local prefixes
+            const uint32_t per = (m + nthreads - 1) / nthreads;
+            const uint32_t i0 = min(m, (uint32_t)tid * per), i1 = min(m, i0 + per);
+            uint32_t mine = 0;
+            for (uint32_t i = i0; i < i1; ++i) mine += entry(i);  // < 2^32: a segment holds < 2^32 bytes
+            uint32_t incl = mine;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += t;
+            }
+            if (lane == 31) s_wsum[warp] = incl;
+            __syncthreads();
+            uint32_t run = incl - mine, segsum = 0;
+            for (int w = 0; w < nwarps; ++w) {
+                if (w < warp) run += s_wsum[w];
+                segsum += s_wsum[w];
+            }
+            for (uint32_t i = i0; i < i1; ++i) {
+                s_pref[i] = run;
+                run += entry(i);
+            }
+            __syncthreads();
+            if (write) {
+                for (uint32_t i = tid; i < m; i += nthreads) {
+                    ws.chunk_off[first + seg + i] = pay0 + carry + s_pref[i];
+                    ws.chunk_size[first + seg + i] = entry(i);
+                }
+            }
+            carry += segsum;
+            __syncthreads();
         }
         if (tid == 0) {
-            if (!code && len - table - 4 * (uint64_t)cnt < payload) code = DEV_E_PAYLOAD_BATCH_TRUNC;  // :127-128
-            if (!code && cnt != g.chunks_in(b)) code = DEV_E_CHUNK_COUNT;  // pipeline.hpp:411-416
-            s_code = code;
-            s_payload = payload;
-        }
-        __syncthreads();
-        code = s_code;
-        if (code) {
-            if (tid == 0) {
+            if (!code && len - pay0 < carry) code = DEV_E_PAYLOAD_BATCH_TRUNC;  // container.cpp:127-128
+            if (!code && !write) code = DEV_E_CHUNK_COUNT;                    // pipeline.hpp:411-416
+            if (code) {
                 record_error(ws.error, first, code);
                 atomicMin(ws.abort_at, (unsigned long long)b);
+            } else {
+                __threadfence();
             }
-            return;
+            s_code = code;
         }
-        uint64_t off = table + 4 * (uint64_t)cnt + before + (incl - mine);
-        for (uint32_t i = i0; i < i1; ++i) {
-            const uint32_t sz = ld_u32_le(arc + table + 4 * (uint64_t)i);
-            ws.chunk_off[first + i] = off;
-            ws.chunk_size[first + i] = sz;
-            off += sz;
-        }
+        __syncthreads();
+        if (s_code) return;
+        // every thread's offset stores are ordered before the release by its own fence
         __threadfence();
         __syncthreads();
         if (tid == 0) st_release32(&ws.ready[b], 1u);
-        cursor = table + 4 * (uint64_t)cnt + s_payload;
-        __syncthreads();
+        cursor = pay0 + carry;
     }
     if (tid == 0 && cursor != len) record_error(ws.error, g.n_chunks, DEV_E_TRAILING);  // pipeline.hpp:460-461
 }
@@ -363,15 +409,18 @@ __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(con
     constexpr int nwarps = NT / 32;
     using SI = slot_info<T, B, nwarps>;
 
-    if (blockIdx.x == 0) {
-        walk_frames(arc, len, g, ws);
-        return;
-    }
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t n = g.chunk_n;
     const int NC = (int)((n - 1) / 8);
     const int BM = NC / 8;  // sparse bitmap bytes (bitplane.hpp:113-122)
     const uint32_t region = decode_region_bytes<T>(n);
+    if (blockIdx.x == 0) {  // the slot ring of block 0 is the walker's table buffer
+        // raw table bytes (4 cap + 32) then cap prefixes
+        const uint32_t cap = ((kDecodeSlots * region) - 48) / 8 & ~3u;
+        walk_frames(arc, len, g, ws, reinterpret_cast<uint4*>(smem),
+                    reinterpret_cast<uint32_t*>(smem + 4 * cap + 32), cap);
+        return;
+    }
 
     __shared__ __align__(8) uint64_t s_full[kDecodeSlots], s_empty[kDecodeSlots];
     __shared__ SI s_info[kDecodeSlots];
