@@ -106,6 +106,25 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def link_bandwidth(torch, dev, host_pinned):
+    """Pinned host<->device copy bandwidth (bytes/s), best of 3, CUDA events."""
+    n = min(host_pinned.numel(), (1 << 30) // host_pinned.element_size())
+    h = host_pinned[:n]
+    d = torch.empty_like(h, device=dev)
+    best = [0.0, 0.0]
+    for _ in range(3):
+        for k, (dst, src) in enumerate(((d, h), (h, d))):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            dst.copy_(src, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            best[k] = max(best[k], h.numel() * h.element_size() / (e0.elapsed_time(e1) / 1e3))
+    del d
+    return best[0], best[1]
+
+
 def cpu_reference_round_trip(values: np.ndarray, steps: int, warmup: int):
     """The unmodified reference (oracle/_ref) compress_pipeline + decompress_pipeline on
     host cores; falls back to the C restatement (single thread) if _ref is absent."""
@@ -272,6 +291,13 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": world * in_bytes * len(times) / te / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": in_bytes + nb_e, "d2h_bytes_per_step": nb_e + in_bytes,
                "ms_per_step": 1e3 * te / len(times)}
+        # the host link bounds this number: pinned copy bandwidth measured on this box, and
+        # the fraction of the link-bound time (compress: H2D of values || D2H of the
+        # archive, then decompress: H2D of the archive || D2H of values) achieved
+        h2d, d2h = link_bandwidth(torch, dev, host_vals)
+        bound_s = max(in_bytes / h2d, nb_e / d2h) + max(nb_e / h2d, in_bytes / d2h)
+        e2e.update({"link_h2d_gbs": h2d / 1e9, "link_d2h_gbs": d2h / 1e9,
+                    "link_frac": bound_s / (te / len(times))})
         del h_arc, h_back
 
     if rank != 0:
