@@ -96,8 +96,11 @@ __device__ __forceinline__ uint32_t nonzero_bytes(uint32_t w) {
     return ((((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w) >> 7) & 0x01010101u;
 }
 
+#ifndef FB_ENC_MIN_BLOCKS
+#define FB_ENC_MIN_BLOCKS 8   // resident CTAs of 128 threads per SM the register budget targets
+#endif
 template <typename T, int NT>
-__global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT : 1))
+__global__ void __launch_bounds__(NT, NT <= 128 ? FB_ENC_MIN_BLOCKS : (2048 / NT > 0 ? 2048 / NT : 1))
     encode_chunks_kernel(const T* __restrict__ in, geometry g, uint8_t* __restrict__ out,
                          uint64_t out_cap, encode_ws ws) {
     using tr = lane_traits<T>;
@@ -154,17 +157,6 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
             for (int j = 0; j < 8; ++j) v[j] = (active && i0 + 1 + j < len) ? __ldg(src + 1 + j) : T(0);
             if (active && i0 < len) vprev = __ldg(src);
         }
-    }
-
-    // zero the image buffer while the loads are in flight: bitmap and payload bytes of
-    // all-zero warp rows then need no store at all
-    {
-        uint4* st = reinterpret_cast<uint4*>(s_stage);
-        constexpr int kWords = (int)(encode_stage_bytes_max<T, NT>() >> 4);
-        const int words = (int)(encode_stage_bytes<T>(n) >> 4);
-#pragma unroll
-        for (int i = tid; i < kWords; i += PT)
-            if (i < words) st[i] = make_uint4(0u, 0u, 0u, 0u);
     }
 
     // ---- analyze, phase 1: warp 0 runs the exact loop on 32 samples spread over the
@@ -459,23 +451,25 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 8 : (2048 / NT > 0 ? 2048 / NT
         }
         // sparse rows (bitplane.hpp:126-148): bitmap byte j nonzero -> bit 7-j%8 of bitmap
         // byte j/8, then the nonzero bytes in order at warp prefix + ballot rank.  The 32
-        // bitmap bytes a warp owns in this block (8 planes x 4) go out in one store; the
-        // buffer is zeroed, so all-zero bytes are skipped.
+        // bitmap bytes a warp owns in this block (8 planes x 4) go out in one store.  Every
+        // image byte below `size` is written (bitmaps always, payloads are contiguous), so
+        // the staging buffer needs no zeroing.
         if (sblk) {
             const uint4 wp = *reinterpret_cast<const uint4*>(&s_wpre[warp * 64 + 8 * sb]);
             const uint32_t wpre[8] = {wp.x & 0xffffu, wp.x >> 16, wp.y & 0xffffu, wp.y >> 16,
                                       wp.z & 0xffffu, wp.z >> 16, wp.w & 0xffffu, wp.w >> 16};
             uint32_t mk[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
+            for (int k = 0; k < 8; ++k) {
                 mk[k] = __ballot_sync(0xffffffffu, ((k < 4 ? ylo >> (8 * k) : yhi >> (8 * (k - 4))) & 0xffu) != 0u);
+            }
             {
                 const int kl = lane >> 2, ql = lane & 3;
                 uint32_t mm = mk[0];
 #pragma unroll
                 for (int k = 1; k < 8; ++k) mm = kl == k ? mk[k] : mm;
                 const uint32_t bm = __brev(mm >> (8 * ql)) >> 24;
-                if (((sblk >> kl) & 1u) && bm != 0u && 4 * warp + ql < BM) s_stage[s_rowoff[8 * sb + kl] + 4 * warp + ql] = (uint8_t)bm;
+                if (((sblk >> kl) & 1u) && 4 * warp + ql < BM) s_stage[s_rowoff[8 * sb + kl] + 4 * warp + ql] = (uint8_t)bm;
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
