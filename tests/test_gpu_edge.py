@@ -1,0 +1,135 @@
+"""GPU parity on inputs aimed at the encoder's fast paths (dpds.cuh lean certification,
+phase-1 sampling, 32-bit delta path, beta_hat from the max high word) and the decoder's
+division-free inverse scale.  Every archive must equal the CPU oracle's byte for byte
+(chunk_codec.hpp:50-74; transform.hpp:47-89) and decode bit-exactly.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2511_04140_b200 import F32, F64
+
+pytestmark = pytest.mark.gpu
+
+N = 1025
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def check(codec, oracle, vals, n=N, bv=N * 8):
+    want = oracle.compress_archive(vals, n, bv)
+    arc, nb = codec.compress_device(dev(vals), chunk_n=n, batch_values=bv)
+    got = arc[:nb].cpu().numpy().tobytes()
+    assert got == want, f"archive differs ({len(got)} vs {len(want)} bytes)"
+    back = codec.decompress_device(arc, nb).cpu().numpy()
+    assert back.view(np.uint8).tobytes() == vals.view(np.uint8).tobytes()
+
+
+def decimals(rng, count, dp, lo=-1e4, hi=1e4, dtype=np.float64):
+    units = rng.integers(int(lo * 10 ** dp), int(hi * 10 ** dp), count)
+    if dtype == np.float64:
+        return (units.astype(np.float64) / 10.0 ** dp).astype(dtype)
+    p = np.float32(1)
+    for _ in range(dp):
+        p = np.float32(p * np.float32(10))
+    return units.astype(np.float32) / p
+
+
+def chunks_with(rng, base, inject, every=N):
+    """base values with `inject(chunk_values, rng)` applied to every chunk."""
+    v = base.copy()
+    for c0 in range(0, len(v), every):
+        inject(v[c0:c0 + every], rng)
+    return v
+
+
+@pytest.mark.parametrize("prec", [F64, F32])
+def test_integers_zeros_and_powers_of_two(codec, oracle, prec):
+    dt = np.float64 if prec == F64 else np.float32
+    rng = np.random.default_rng(1)
+    v = rng.integers(-300, 300, 40 * N).astype(dt)            # many zeros, 1, 2, 4, ... 256
+    v[::7] = 0.0
+    v[3::11] = np.array([0.5, 0.25, 1024.0, 2.0 ** -3], dt)[rng.integers(0, 4, len(v[3::11]))]
+    check(codec, oracle, v)
+
+
+@pytest.mark.parametrize("prec", [F64, F32])
+def test_decade_boundaries(codec, oracle, prec):
+    dt = np.float64 if prec == F64 else np.float32
+    rng = np.random.default_rng(2)
+    ks = range(-6, 10) if prec == F64 else range(-3, 5)
+    edge = []
+    for k in ks:
+        x = dt(float(f"1e{k}"))
+        edge += [x, np.nextafter(x, dt(np.inf)), np.nextafter(x, dt(-np.inf)), -x]
+    edge = np.array(edge, dt)
+    # chunks whose max |v| sits exactly on / next to a decade (beta_hat's second pass)
+    v = decimals(rng, 30 * N, 2, -99, 99, dt)
+    v[::N] = edge[rng.integers(0, len(edge), len(v[::N]))]
+    v[5::37] = edge[rng.integers(0, len(edge), len(v[5::37]))]
+    check(codec, oracle, v)
+
+
+@pytest.mark.parametrize("prec", [F64, F32])
+def test_rare_finer_value_not_in_the_sample(codec, oracle, prec):
+    # phase 1 samples indices 32L + 16; a finer decimal elsewhere must still raise alpha_max
+    dt = np.float64 if prec == F64 else np.float32
+    rng = np.random.default_rng(3)
+    fine = decimals(rng, 30 * N, 5 if prec == F64 else 4, -50, 50, dt)
+    base = decimals(rng, 30 * N, 1, -500, 500, dt)
+
+    def inject(c, r):
+        i = int(r.integers(0, len(c)))
+        if i % 32 != 16:
+            c[i] = fine[i]
+    check(codec, oracle, chunks_with(rng, base, inject))
+
+
+@pytest.mark.parametrize("prec", [F64, F32])
+def test_single_exception_makes_case2(codec, oracle, prec):
+    dt = np.float64 if prec == F64 else np.float32
+    rng = np.random.default_rng(4)
+    base = decimals(rng, 24 * N, 2, -1e3, 1e3, dt)
+    specials = np.array([np.nan, np.inf, -0.0, 1e-310 if prec == F64 else 1e-40, np.pi, -np.e], dt)
+
+    def inject(c, r):
+        c[int(r.integers(0, len(c)))] = specials[int(r.integers(0, len(specials)))]
+    check(codec, oracle, chunks_with(rng, base, inject))
+
+
+def test_wide_f64_integers_and_significand_limits(codec, oracle):
+    rng = np.random.default_rng(5)
+    v = np.concatenate([
+        rng.integers(-(10 ** 14), 10 ** 14, 8 * N).astype(np.float64),       # beta near 15
+        rng.integers(10 ** 15, 10 ** 16, 4 * N).astype(np.float64),          # beta 16: Case 2
+        rng.integers(-(10 ** 12), 10 ** 12, 8 * N).astype(np.float64) / 1e3,  # 15 significant digits
+        rng.integers(-(2 ** 40), 2 ** 40, 8 * N).astype(np.float64) / 1e9,
+    ])
+    check(codec, oracle, v)
+
+
+@pytest.mark.parametrize("dp", [0, 3, 7, 12, 18, 21])
+def test_scales_up_to_the_division_free_limit(codec, oracle, dp):
+    rng = np.random.default_rng(6 + dp)
+    mag = 10.0 ** max(0, 14 - dp)
+    v = decimals(rng, 12 * N, dp, -mag, mag) if dp <= 12 else \
+        rng.integers(-10 ** 6, 10 ** 6, 12 * N).astype(np.float64) / 10.0 ** dp
+    check(codec, oracle, v)
+
+
+def test_alpha_22_takes_the_checked_division(codec, oracle):
+    rng = np.random.default_rng(7)
+    v = rng.integers(1, 10 ** 6, 6 * N).astype(np.float64) / 1e22
+    check(codec, oracle, v)
+
+
+def test_deltas_crossing_the_32_bit_path(codec, oracle):
+    # lane integers right around 2^29..2^31 after scaling: the encoder's 32-bit delta path
+    # must hand over to 64-bit arithmetic exactly where the integers stop fitting
+    rng = np.random.default_rng(8)
+    base = rng.integers(2 ** 28, 2 ** 31 + 2 ** 28, 20 * N).astype(np.float64)
+    sign = np.where(rng.integers(0, 2, len(base)) == 1, -1.0, 1.0)
+    v = base * sign / 100.0
+    check(codec, oracle, v)
