@@ -159,14 +159,19 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? FB_ENC_MIN_BLOCKS : (2048 / NT
         }
     }
 
-    // ---- analyze, phase 1: warp 0 runs the exact loop on 32 samples spread over the
-    //      chunk -> A0 = the largest sampled alpha (attained, so alpha_max >= A0) ----
+    // ---- analyze, phase 1: warp 0 runs the exact loop on 32 samples of its own values
+    //      (value 8L + 4 of lane L: no extra load on the critical path) -> A0 = the
+    //      largest sampled alpha (attained, so alpha_max >= A0); lane 0 also prepares
+    //      the chunk-uniform certification parameters for everybody ----
+    __shared__ cert_params<T> s_cp;
     if (warp == 0) {
-        const uint32_t si = (uint32_t)lane * (n >> 5) + (n >> 6);
-        const T sv = si < len ? __ldg(in + v0 + si) : T(0);
-        const int a = dp_alpha_k<T, 4>(sv);
+        const int a = dp_alpha_k<T, 4>(v[3]);
         const uint32_t f1 = __reduce_or_sync(0xffffffffu, a < 0 ? 0x80000000u : (1u << a));
-        if (lane == 0) s_flag1[0] = f1;
+        if (lane == 0) {
+            s_flag1[0] = f1;
+            const int a0 = (f1 & 0x7fffffffu) ? 31 - __clz((int)(f1 & 0x7fffffffu)) : 0;
+            s_cp = cert_params_for(T{}, a0);
+        }
     }
     __syncthreads();
     uint32_t F = s_flag1[0];
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? FB_ENC_MIN_BLOCKS : (2048 / NT
     uint32_t f2 = 0;     // exception bit | one-hot alphas of values decided by the exact loop
     uint32_t mx = 0;     // max |v| high word (f32: bits) -> floor_log10(max|v|) for beta_hat
     if (active && !(F >> 31)) {
-        const cert_params<T> cp = cert_params_for(T{}, A0);
+        const cert_params<T> cp = s_cp;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             uint32_t ah;
