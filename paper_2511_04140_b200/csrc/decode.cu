@@ -1,19 +1,22 @@
-// decode.cu -- single-launch Falcon decompress for sm_100a.
+// decode.cu -- single-launch Falcon decompress for sm_100a (persistent, warp-specialised).
 //
 // The archive has no batch index (FORMAT.md:10-14): batch b+1's frame starts where
-// batch b's payload ends, so frames must be located sequentially.  Ticket 0 of the
-// launch is a *frame walker* CTA that runs the read_batch chain (container.cpp:113-132,
-// pipeline.hpp:394-417): it validates each frame, scans its u32 size table into
-// per-chunk offsets and publishes the batch.  Every other ticket decodes one chunk as
-// soon as its batch is published, so the walk overlaps the decode of earlier batches.
-//
-// Per chunk (decompress_chunk, chunk_codec.hpp:86-122):
-//   stage   chunk bytes -> smem with 16-B vector loads at the source's 16-B phase
-//   parse   header + flag + row-walk validation in reference check order (warp 0)
-//   rows    dense rows copied, sparse rows expanded with ballot ranks (one warp/row)
-//   planes  thread t owns byte column t: 8x8 transposes rebuild lanes 8t..8t+7
-//   scan    block-wide wrapping inclusive scan of unzigzagged deltas (transform.hpp:91-106)
-//   values  Case 1: (T)g / 10^alpha (IEEE division), Case 2: raw bits; coalesced stores
+// batch b's payload ends, so frames must be located sequentially.  Block 0 of the launch
+// is the *frame walker* (read_batch chain, container.cpp:113-132, pipeline.hpp:394-417):
+// per batch it loads the size table with vector loads, validates the frame, scans it
+// into per-chunk offsets and publishes the batch.  In every other block:
+//   producers (2 warps)  take chunk tickets, wait for the chunk's batch, stage the chunk
+//                        bytes into a smem slot ring (cp.async at the 16-B phase), and
+//                        parse + validate it in the reference's check order
+//                        (chunk_codec.hpp:86-122, bitplane.hpp:152-186): row offsets,
+//                        dense mask, per-warp sparse payload prefixes, scale constants
+//   consumers (NT thr.)  thread t owns byte column t: gathers byte t of every row (dense
+//                        rows verbatim; sparse rows: bitmap bit + ballot rank), 8x8 bit
+//                        transposes + PRMT byte transposes rebuild lanes 8t..8t+7, a
+//                        block-wide wrapping scan of unzigzagged deltas
+//                        (transform.hpp:91-106), RN(g / 10^alpha) without a division
+//                        (dpds.cuh) or the raw bits, and lane-contiguous value stores
+//                        through the slot
 #include "dpds.cuh"
 #include "falcon_common.cuh"
 #include "kernels.h"
@@ -195,12 +198,8 @@ __device__ __forceinline__ bool mbar_try_suspend(uint64_t* bar, uint32_t parity)
     return done != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-#ifdef FB_AB_SPIN
-    while (!mbar_try(bar, parity)) __nanosleep(32);
-#else
     while (!mbar_try_suspend(bar, parity)) {
     }
-#endif
 }
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
@@ -315,23 +314,6 @@ __device__ __forceinline__ void parse_chunk(const uint8_t* p, const uint8_t* hp,
                                            : __popc(dm0) + __popc(dm1 & ((1u << (r - 32)) - 1u));
                 const uint32_t rp = pos0 + nd * (uint32_t)NC + acc;
                 if (size < rp + (uint32_t)BM) { bad = r; bad_code = DEV_E_BITMAP_TRUNC; break; }
-#ifdef FB_AB_OLDPARSE
-                uint32_t pc = 0;
-                const uint32_t g0 = 4u * (uint32_t)lane;
-                if (lane < NW) {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (g0 + k < (uint32_t)BM) pc += __popc(p[rp + g0 + k]);
-                }
-                uint32_t incl = pc;
-#pragma unroll
-                for (int d = 1; d < NW; d <<= 1) {
-                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
-                    if (lane >= d) incl += t;
-                }
-                const uint32_t tot = __shfl_sync(0xffffffffu, incl, NW - 1);
-                if (lane < NW) si.wpre[lane * 64 + (w - 1 - r)] = (uint16_t)(incl - pc);
-#else
                 // chain: one bitmap byte per lane, popcounts summed by REDUX (the next
                 // sparse row's offset needs only the total)
                 const uint32_t pa = lane < BM ? __popc(p[rp + lane]) : 0u;
@@ -361,7 +343,6 @@ __device__ __forceinline__ void parse_chunk(const uint8_t* p, const uint8_t* hp,
                     }
                     if (lane < NW) si.wpre[lane * 64 + (w - 1 - r)] = (uint16_t)(incl - gs);
                 }
-#endif
                 if (size - rp - (uint32_t)BM < tot) { bad = r; bad_code = DEV_E_PAYLOAD_TRUNC; break; }
                 if (r0 > r) acc0 += (uint32_t)BM + tot;
                 if (r1 > r) acc1 += (uint32_t)BM + tot;
@@ -682,17 +663,6 @@ __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(con
     // lane-contiguous stores: a warp writes 256 consecutive bytes per instruction instead
     // of 32 scattered 8-B pieces.
     T* dst = out + v0;
-#ifdef FB_AB_DIRECT_STORE
-    const uint32_t i0 = 8u * (uint32_t)tid + 1u;
-    auto store = [&](auto to_value) {
-        if (active) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (i0 + j < count) dst[i0 + j] = to_value((B)(before + d[j]));
-        }
-        if (tid == 0 && count > 0) dst[0] = to_value(z1);
-    };
-#else
     T* vstage = reinterpret_cast<T*>(smem + (size_t)sl * region);
     constexpr uint32_t SP = NT + 2;  // decode_stage_stride(NT)
     auto store = [&](auto to_value) {
@@ -700,12 +670,7 @@ __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(con
         for (int j = 0; j < 8; ++j) vstage[j * SP + tid] = to_value((B)(before + d[j]));
         if (tid == 0) vstage[8 * SP] = to_value(z1);
     };
-#endif
-#ifdef FB_AB_NO_MARKSTEIN
-    constexpr int kMark = -1;
-#else
     constexpr int kMark = sizeof(T) == 8 ? kMarksteinMaxAlpha64 : kMarksteinMaxAlpha32;
-#endif
     if (case2) {
         store([&](B gv) -> T { return value_of(unzigzag<B>(gv)); });
     } else if ((int)hA <= kMark) {
@@ -713,7 +678,6 @@ __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(con
     } else {
         store([&](B gv) -> T { return inverse_scale_rn(from_i64(T{}, (long long)(S)gv), scale, rscale); });
     }
-#ifndef FB_AB_DIRECT_STORE
     consumer_sync<NT>();
     {
         // value i = tid + NT m (m = 0..8) is lane k = i - 1: thread k / 8, register k % 8;
@@ -726,7 +690,6 @@ __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(con
             if (m * NT < 8u * NT + 1u && i < count) dst[i] = i == 0 ? vstage[8 * SP] : vsrc[(NT / 8) * m];
         }
     }
-#endif
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sl]);

@@ -1,26 +1,28 @@
-// encode.cu -- fused single-pass Falcon compress for sm_100a.
+// encode.cu -- Falcon compress for sm_100a: encode_chunks_kernel + place_chunks_kernel.
 //
-// One CTA encodes one chunk (chunk_n values: z1 + (chunk_n-1) delta lanes) straight
-// into its final archive position.  Thread t owns the "byte column" t: delta lanes
-// 8t..8t+7 (values 8t+1..8t+8), which is exactly byte t of every bit-plane row
-// (FORMAT.md:79-84), so planes come out of per-thread 8x8 bit transposes.
+// encode_chunks_kernel: one CTA per chunk (chunk_n values: z1 + (chunk_n-1) delta
+// lanes).  Thread t owns the "byte column" t: delta lanes 8t..8t+7 (values 8t+1..8t+8),
+// which is exactly byte t of every bit-plane row (FORMAT.md:79-84), so planes come out of
+// per-thread 8x8 bit transposes.
 //
 //   load     each thread loads its 8 values + the preceding one into registers
-//   analyze  phase 1: exact dp_ds loop on one sample value per thread -> A0 = max
-//            phase 2: every value certified against A0 (dpds.cuh (3)); the few that
-//            cannot be certified run the exact loop.  alpha_max, exceptions, max|v|
-//            (numeric.hpp:108-140, transform.hpp:47-68) -- bit-identical results
-//   delta    g = round(v*10^alpha_max) (reused from certification) or
-//            zigzag(bits(v)); z = zigzag(g_i - g_{i-1}) (transform.hpp:72-89)
-//   planes   per 8 bit positions: 8x8 bit transpose -> this thread's row bytes
-//   size     warp 0: per-row zero-byte counts, dense/sparse choice, row offsets
-//            (bitplane.hpp:113-122, chunk_codec.hpp:59-73), decoupled look-back over
-//            chunk sizes in ticket order; batch-frame tables are added analytically
-//   emit     one warp per row into smem staging at the destination's 16-B phase:
-//            dense rows copied, sparse rows compacted with ballot ranks
-//   store    16-B vector stores; bytes only at the two ragged ends
+//   analyze  phase 1: warp 0 runs the exact dp_ds loop on 32 samples -> A0 (attained)
+//            phase 2: every value gets the one-sided lean certification at A0
+//            (dpds.cuh); the few it cannot decide run the exact loop.  alpha_max,
+//            exceptions, max|v| (numeric.hpp:108-140, transform.hpp:47-68), bit-exact
+//   delta    Case 1 reuses the certified lane integers, Case 2 zigzags the bits;
+//            z = zigzag(g_i - g_{i-1}) (transform.hpp:72-89), 32-bit when it fits
+//   planes   per 8 bit positions: PRMT gather + 8x8 bit transpose -> the thread's row
+//            bytes; nonzero-byte counts per plane by REDUX
+//   size     warp 0: dense/sparse choice per row, row offsets, chunk size
+//            (bitplane.hpp:113-122, chunk_codec.hpp:59-73)
+//   emit     every thread writes its column of every row into the smem image (sparse
+//            rows: bitmap bytes + payload at warp prefix + ballot rank,
+//            bitplane.hpp:126-148); 16-B stores into the chunk's scratch slot
 //
-// frame_tables_kernel then writes the [u32 count][u32 size...] tables and the header.
+// place_chunks_kernel: scan of the chunk sizes in tiles with a decoupled look-back, then
+// the images are copied to their archive offsets and the batch tables and the header
+// are written (container.cpp:44-55, 88-111).
 #include "dpds.cuh"
 #include "falcon_common.cuh"
 #include "kernels.h"
