@@ -187,7 +187,7 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
-    from paper_2511_04140_b200 import Codec, compress_bound, options
+    from paper_2511_04140_b200 import Codec, compress_bound, options, read_header
 
     kind, prec, n, dp, desc = WORKLOADS[args.workload]
     tdt = torch.float64 if prec == 0 else torch.float32
@@ -205,22 +205,32 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
 
-    def step(evs=None):
+    d_nb = torch.zeros(1, dtype=torch.int64, device=dev)   # archive length, device-resident
+
+    def step(evs=None, chained=True):
+        """One pass of the hot path: compress the workload, then decompress the archive.
+        The timed steps chain the two on the stream with no host round trip (the archive
+        length stays on the device); device errors are collected by codec.sync()."""
         if evs is not None:
             codec.set_kernel_events(enc=(evs[0], evs[1]), dec=(evs[2], evs[3]))
-        _, nb = codec.compress_device(d_vals, CHUNK_N, BATCH_VALUES, out=d_arc, stream=sh)
+        if not chained:
+            _, nb = codec.compress_device(d_vals, CHUNK_N, BATCH_VALUES, out=d_arc, stream=sh)
+            codec.decompress_device(d_arc, nb, out=d_back, stream=sh)
+            return nb
+        codec.compress_device_async(d_vals, d_arc, d_nb, CHUNK_N, BATCH_VALUES, stream=sh)
         if world > 1:
             # the one exchange step of a sharded archive: every rank's byte total, so
             # shard g lands at 47 + sum_{h<g} (bytes_h - 47) when concatenated (SURVEY 8e)
             sizes = torch.zeros(world, dtype=torch.int64, device=dev)
-            sizes[rank] = nb
+            sizes[rank] = d_nb[0]
             dist.all_reduce(sizes)
-        codec.decompress_device(d_arc, nb, out=d_back, stream=sh)
-        return nb
+        codec.decompress_device_chained(d_arc, d_nb, info, d_back, stream=sh)
+        return None
 
-    # correctness gate before timing: round trip must be bit-exact
-    nb = step()
+    # correctness gate before timing: round trip must be bit-exact (synchronous API)
+    nb = step(chained=False)
     torch.cuda.synchronize()
+    info = read_header(d_arc[:47].cpu().numpy().tobytes())
     assert torch.equal(d_back.view(torch.int64 if prec == 0 else torch.int32),
                        d_vals.view(torch.int64 if prec == 0 else torch.int32)), "round trip mismatch"
     ratio = nb / (n * esz)
@@ -246,6 +256,8 @@ def run_ours(args, rank, world, local_rank):
         step(kev[k])
     t1.record(stream)
     torch.cuda.synchronize()
+    codec.sync(sh)   # raises on any device-side error of the timed steps
+    assert int(d_nb.item()) == nb, "chained steps produced a different archive length"
     if world > 1:
         dist.barrier()
     time.sleep(0.1)

@@ -138,6 +138,13 @@ falcon_status falcon_decompress_device_async(falcon_ctx* ctx, int precision,
                                              const void* d_archive, uint64_t archive_bytes,
                                              const falcon_archive_info* info, void* d_values,
                                              uint64_t cap_values, void* stream);
+/* Chained form: the archive length is read on the device from d_archive_bytes (e.g. the
+ * d_out_bytes of falcon_compress_device_async on the same stream), so a compress ->
+ * decompress chain runs without a host round trip.  Errors surface in falcon_ctx_sync(). */
+falcon_status falcon_decompress_device_chained(falcon_ctx* ctx, int precision, const void* d_archive,
+                                               const uint64_t* d_archive_bytes,
+                                               const falcon_archive_info* info, void* d_values,
+                                               uint64_t cap_values, void* stream);
 /* Profiling hook: when set (non-null), device-resident calls on ctx record enc_start /
  * enc_stop right before / after the encode kernel and dec_start / dec_stop around the
  * decode kernel, on the call's stream.  Pass nulls to clear. */

@@ -114,7 +114,7 @@ falcon_status parse_header(const uint8_t* in, uint64_t len, falcon_archive_info*
 
 falcon_status enqueue_decompress(falcon_ctx* ctx, int prec, const void* d_archive, uint64_t bytes,
                                  const falcon_archive_info* info, void* d_values, uint64_t cap,
-                                 cudaStream_t st, geometry& g) {
+                                 cudaStream_t st, geometry& g, const uint64_t* d_bytes = nullptr) {
     if (info->precision != prec)
         return set_error(FALCON_ERR_INVALID, "archive precision does not match the requested value type");
     if (info->total_values > cap)
@@ -124,8 +124,8 @@ falcon_status enqueue_decompress(falcon_ctx* ctx, int prec, const void* d_archiv
                          "chunk_n > 4097 is not supported by the sm_100a kernels of this build");
     FB_TRY(make_geometry(info->total_values, info->chunk_n, info->batch_values ? info->batch_values : 1,
                          47, g));
-    if (g.n_chunks == 0) {
-        if (bytes != 47) return set_error(FALCON_ERR_CORRUPT, "trailing bytes after final batch");
+    if (g.n_chunks == 0) {  // (a chained call cannot check the length of an empty archive)
+        if (!d_bytes && bytes != 47) return set_error(FALCON_ERR_CORRUPT, "trailing bytes after final batch");
         return FALCON_OK;
     }
     FB_TRY(ctx->dec_off.ensure(g.n_chunks * sizeof(uint64_t)));
@@ -135,10 +135,10 @@ falcon_status enqueue_decompress(falcon_ctx* ctx, int prec, const void* d_archiv
     cudaError_t e = prec == FALCON_F64
                         ? launch_decode<double>(static_cast<const uint8_t*>(d_archive), bytes, g,
                                                 static_cast<double*>(d_values), ws, st,
-                                                ctx->prof_ev[2], ctx->prof_ev[3])
+                                                ctx->prof_ev[2], ctx->prof_ev[3], d_bytes)
                         : launch_decode<float>(static_cast<const uint8_t*>(d_archive), bytes, g,
                                                static_cast<float*>(d_values), ws, st,
-                                               ctx->prof_ev[2], ctx->prof_ev[3]);
+                                               ctx->prof_ev[2], ctx->prof_ev[3], d_bytes);
     if (e != cudaSuccess) return set_error(FALCON_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
     return FALCON_OK;
 }
@@ -259,6 +259,18 @@ falcon_status falcon_decompress_device_async(falcon_ctx* ctx, int precision,
     geometry g;
     return enqueue_decompress(ctx, precision, d_archive, archive_bytes, info, d_values, cap_values,
                               static_cast<cudaStream_t>(stream), g);
+}
+
+falcon_status falcon_decompress_device_chained(falcon_ctx* ctx, int precision, const void* d_archive,
+                                               const uint64_t* d_archive_bytes,
+                                               const falcon_archive_info* info, void* d_values,
+                                               uint64_t cap_values, void* stream) {
+    if (!ctx || !info || !d_archive_bytes) return set_error(FALCON_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lock(ctx->api_mutex);
+    device_guard dg(ctx->device);
+    geometry g;
+    return enqueue_decompress(ctx, precision, d_archive, 0, info, d_values, cap_values,
+                              static_cast<cudaStream_t>(stream), g, d_archive_bytes);
 }
 
 falcon_status falcon_decompress_device(falcon_ctx* ctx, int precision, const void* d_archive,

@@ -380,9 +380,11 @@ __device__ __forceinline__ void parse_chunk(const uint8_t* p, const uint8_t* hp,
 // only gather, scan and store.  Staging and parsing of later chunks overlap the decode
 // of the current one; the next chunk's offsets are fetched while a copy is in flight.
 template <typename T, int NT>
-__global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(const uint8_t* __restrict__ arc, uint64_t len,
+__global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(const uint8_t* __restrict__ arc, uint64_t len_arg,
+                                                                const uint64_t* __restrict__ d_len,
                                                                 geometry g, T* __restrict__ out,
                                                                 decode_ws ws) {
+    const uint64_t len = d_len ? *d_len : len_arg;
     using tr = lane_traits<T>;
     using B = typename tr::B;
     using S = typename tr::S;
@@ -703,7 +705,8 @@ uint32_t decode_smem_bytes(uint32_t chunk_n) {
 
 template <typename T>
 cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry& g, T* d_out,
-                          const decode_ws& ws, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1) {
+                          const decode_ws& ws, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1,
+                          const uint64_t* d_len) {
     cudaError_t e;
     if (g.n_chunks == 0) return cudaSuccess;
     if ((e = cudaMemsetAsync(ws.ticket, 0, sizeof(uint32_t), st))) return e;
@@ -711,7 +714,7 @@ cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry
     if ((e = cudaMemsetAsync(ws.abort_at, 0xff, sizeof(unsigned long long), st))) return e;
     const uint32_t threads = encode_block_threads(g.chunk_n);
     const uint32_t smem = decode_smem_bytes<T>(g.chunk_n);
-    void (*kern)(const uint8_t*, uint64_t, geometry, T*, decode_ws);
+    void (*kern)(const uint8_t*, uint64_t, const uint64_t*, geometry, T*, decode_ws);
     switch (threads) {
     case 32: kern = decode_chunks_kernel<T, 32>; break;
     case 64: kern = decode_chunks_kernel<T, 64>; break;
@@ -737,15 +740,17 @@ cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry
     if (grid > g.n_chunks + 1) grid = g.n_chunks + 1;
     if (grid < 2) grid = 2;
     if (ev0 && (e = cudaEventRecord(ev0, st))) return e;
-    kern<<<(unsigned)grid, threads + 32 * kProducers, smem, st>>>(d_archive, len, g, d_out, ws);
+    kern<<<(unsigned)grid, threads + 32 * kProducers, smem, st>>>(d_archive, len, d_len, g, d_out, ws);
     if ((e = cudaGetLastError())) return e;
     return ev1 ? cudaEventRecord(ev1, st) : cudaSuccess;
 }
 
 template cudaError_t launch_decode<double>(const uint8_t*, uint64_t, const geometry&, double*,
-                                           const decode_ws&, cudaStream_t, cudaEvent_t, cudaEvent_t);
+                                           const decode_ws&, cudaStream_t, cudaEvent_t, cudaEvent_t,
+                                           const uint64_t*);
 template cudaError_t launch_decode<float>(const uint8_t*, uint64_t, const geometry&, float*,
-                                          const decode_ws&, cudaStream_t, cudaEvent_t, cudaEvent_t);
+                                          const decode_ws&, cudaStream_t, cudaEvent_t, cudaEvent_t,
+                                          const uint64_t*);
 template uint32_t decode_smem_bytes<double>(uint32_t);
 template uint32_t decode_smem_bytes<float>(uint32_t);
 

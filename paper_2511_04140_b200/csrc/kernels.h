@@ -53,10 +53,11 @@ cudaError_t launch_encode(const T* d_in, const geometry& g, uint8_t* d_out, uint
                           cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 
 // d_archive points at the archive's first byte (the 47-byte header), `len` bytes long.
+// d_len (optional): the archive length in device memory, read by the kernel instead of len.
 template <typename T>
 cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry& g, T* d_out,
                           const decode_ws& ws, cudaStream_t st, cudaEvent_t ev0 = nullptr,
-                          cudaEvent_t ev1 = nullptr);
+                          cudaEvent_t ev1 = nullptr, const uint64_t* d_len = nullptr);
 
 cudaError_t launch_selftest_dp(int prec, const void* v, uint64_t n, int A, int8_t* full,
                                int8_t* lit, int8_t* cert, int64_t* g, cudaStream_t st);

@@ -26,6 +26,7 @@ EXPORTED = [
     "falcon_ctx_destroy", "falcon_max_encoded_chunk_size", "falcon_compress_bound",
     "falcon_write_header", "falcon_read_header", "falcon_compress_device",
     "falcon_compress_device_async", "falcon_decompress_device", "falcon_decompress_device_async",
+    "falcon_decompress_device_chained",
     "falcon_ctx_sync", "falcon_compress_stream", "falcon_decompress_stream", "falcon_compress_host",
     "falcon_decompress_host", "falcon_compress_chunk", "falcon_decompress_chunk", "falcon_synth_fill",
     "falcon_ctx_set_kernel_events", "falcon_selftest_dp", "falcon_selftest_div",
@@ -103,6 +104,7 @@ def load() -> C.CDLL:
     L.falcon_compress_device_async.argtypes = [vp, i32, vp, u64, u32, u64, vp, u64, vp, vp]
     L.falcon_decompress_device.argtypes = [vp, i32, vp, u64, vp, u64, C.POINTER(u64), vp]
     L.falcon_decompress_device_async.argtypes = [vp, i32, vp, u64, C.POINTER(ArchiveInfo), vp, u64, vp]
+    L.falcon_decompress_device_chained.argtypes = [vp, i32, vp, vp, C.POINTER(ArchiveInfo), vp, u64, vp]
     L.falcon_ctx_sync.argtypes = [vp, vp]
     L.falcon_ctx_set_kernel_events.argtypes = [vp, vp, vp, vp, vp]
     L.falcon_selftest_dp.argtypes = [vp, i32, vp, u64, i32, vp, vp, vp, vp, vp]
@@ -238,6 +240,16 @@ class Codec:
         _check(self.lib.falcon_decompress_device(self.ctx, prec, C.c_void_p(archive.data_ptr()), nbytes,
                                                  C.c_void_p(out.data_ptr()), out.numel(), C.byref(nv), st))
         return out[: nv.value]
+
+    def decompress_device_chained(self, archive, nbytes_dev, info: ArchiveInfo, out, stream=None):
+        """Decode with the archive length read on the device (nbytes_dev: a CUDA uint64/int64
+        tensor, e.g. the out_bytes of compress_device_async): no host round trip."""
+        import torch
+        st = C.c_void_p(stream if stream is not None else torch.cuda.current_stream(archive.device).cuda_stream)
+        _check(self.lib.falcon_decompress_device_chained(
+            self.ctx, prec_of(out.dtype), C.c_void_p(archive.data_ptr()), C.c_void_p(nbytes_dev.data_ptr()),
+            C.byref(info), C.c_void_p(out.data_ptr()), out.numel(), st))
+        return out
 
     def decompress_device_async(self, archive, nbytes: int, info: ArchiveInfo, out, stream=None):
         import torch

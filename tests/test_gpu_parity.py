@@ -231,3 +231,24 @@ def test_large_outlier_round_trip_and_ratio(codec, oracle):
 def test_unsupported_chunk_n_fails_loudly(codec):
     with pytest.raises(FalconError, match="not supported"):
         codec.compress_device(dev(np.zeros(9000)), chunk_n=8193, batch_values=9000)
+
+
+def test_chained_device_round_trip_without_host_sync(codec, oracle):
+    # compress_device_async leaves the archive length on the device; the chained decoder
+    # reads it there, so the pair runs back to back on one stream
+    from paper_2511_04140_b200 import compress_bound, read_header
+    vals = synth("outlier", 200_000, F64, dp=2, seed=41, period=100)
+    want = oracle.compress_archive(vals, 1025, 1025 * 16)
+    d = dev(vals)
+    arc = torch.empty(compress_bound(F64, len(vals), 1025, 1025 * 16), dtype=torch.uint8, device="cuda")
+    d_nb = torch.zeros(1, dtype=torch.int64, device="cuda")
+    back = torch.empty_like(d)
+    info = read_header(want[:47])
+    for _ in range(3):
+        back.zero_()
+        codec.compress_device_async(d, arc, d_nb, 1025, 1025 * 16)
+        codec.decompress_device_chained(arc, d_nb, info, back)
+    codec.sync()
+    assert int(d_nb.item()) == len(want)
+    assert arc[: len(want)].cpu().numpy().tobytes() == want
+    assert bits(back.cpu().numpy()) == bits(vals)
