@@ -605,42 +605,58 @@ __global__ void __launch_bounds__(kPlaceTile) place_chunks_kernel(geometry g, ui
         for (int i = 0; i < 47; ++i) out[i] = hdr.b[i];
     }
 
-    // copy: each warp moves its 32 chunks, one after another
-    for (int k = 0; k < 32; ++k) {
+    // copy: each warp moves its 32 chunks as one flat list of destination vectors, so a
+    // lane's consecutive vectors are independent (their loads overlap) instead of the
+    // chunks being copied one after another
+    __shared__ uint32_t s_vpre[kPlaceTile / 32][33];
+    {
+        const int idx = warp * 32 + lane;
+        const uint64_t cc = t * kPlaceTile + idx;
+        uint32_t nv = 0;
+        if (cc < g.n_chunks) {
+            const uint64_t off = s_off[idx];
+            const uint32_t size = s_sz[idx];
+            if (off + size > out_cap) record_error(ws.error, cc, DEV_E_CAPACITY);
+            else nv = ((uint32_t)(off & 15) + size + 15) >> 4;
+        }
+        uint32_t incl = nv;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += x;
+        }
+        s_vpre[warp][lane] = incl - nv;
+        if (lane == 31) s_vpre[warp][32] = incl;
+        __syncwarp();
+    }
+    const uint32_t V = s_vpre[warp][32];
+    int k = 0;  // this lane's current chunk (vectors are visited in increasing order)
+    for (uint32_t gv = lane; gv < V; gv += 32) {
+        while (gv >= s_vpre[warp][k + 1]) ++k;
         const int idx = warp * 32 + k;
         const uint64_t cc = t * kPlaceTile + idx;
-        if (cc >= g.n_chunks) break;
         const uint64_t off = s_off[idx];
         const uint32_t size = s_sz[idx];
-        if (off + size > out_cap) {
-            if (lane == 0) record_error(ws.error, cc, DEV_E_CAPACITY);
-            continue;
-        }
         const uint32_t* img = reinterpret_cast<const uint32_t*>(ws.images + cc * (uint64_t)ws.slot);
         const uint32_t a = (uint32_t)(off & 15);
         uint8_t* dstb = out + (off - a);
         const uint32_t end = a + size;
-        const uint32_t nvec = (end + 15) >> 4;
-        for (uint32_t vv = lane; vv < nvec; vv += 32) {
-            const uint32_t lo = vv << 4, hi = lo + 16;
-            if (lo >= a && hi <= end) {
-                // destination bytes [lo, lo+16) = image bytes [lo - a, lo - a + 16)
-                const uint32_t sb = lo - a;
-                const uint32_t w0 = sb >> 2, sh = (sb & 3) * 8;
-                uint32_t r[5];
+        const uint32_t vv = gv - s_vpre[warp][k];
+        const uint32_t lo = vv << 4, hi = lo + 16;
+        if (lo >= a && hi <= end) {
+            // destination bytes [lo, lo+16) = image bytes [lo - a, lo - a + 16)
+            const uint32_t sb = lo - a;
+            const uint32_t w0 = sb >> 2, sh = (sb & 3) * 8;
+            uint32_t r[5];
 #pragma unroll
-                for (int i = 0; i < 5; ++i) r[i] = __ldg(img + w0 + i);
-                uint4 o;
-                o.x = __funnelshift_r(r[0], r[1], sh);
-                o.y = __funnelshift_r(r[1], r[2], sh);
-                o.z = __funnelshift_r(r[2], r[3], sh);
-                o.w = __funnelshift_r(r[3], r[4], sh);
-                *reinterpret_cast<uint4*>(dstb + lo) = o;
-            } else {
-                const uint8_t* ib = reinterpret_cast<const uint8_t*>(img);
-                const uint32_t from = lo > a ? lo : a, to = hi < end ? hi : end;
-                for (uint32_t i = from; i < to; ++i) dstb[i] = ib[i - a];
-            }
+            for (int i = 0; i < 5; ++i) r[i] = __ldg(img + w0 + i);
+            *reinterpret_cast<uint4*>(dstb + lo) =
+                make_uint4(__funnelshift_r(r[0], r[1], sh), __funnelshift_r(r[1], r[2], sh),
+                           __funnelshift_r(r[2], r[3], sh), __funnelshift_r(r[3], r[4], sh));
+        } else {
+            const uint8_t* ib = reinterpret_cast<const uint8_t*>(img);
+            const uint32_t from = lo > a ? lo : a, to = hi < end ? hi : end;
+            for (uint32_t i = from; i < to; ++i) dstb[i] = ib[i - a];
         }
     }
 }
