@@ -140,11 +140,26 @@ falcon_status falcon_decompress_device_async(falcon_ctx* ctx, int precision,
                                              uint64_t cap_values, void* stream);
 /* Chained form: the archive length is read on the device from d_archive_bytes (e.g. the
  * d_out_bytes of falcon_compress_device_async on the same stream), so a compress ->
- * decompress chain runs without a host round trip.  Errors surface in falcon_ctx_sync(). */
+ * decompress chain runs without a host round trip (device-resident form of
+ * decompress_pipeline, pipeline.hpp:370-373).  Errors surface in falcon_ctx_sync(). */
 falcon_status falcon_decompress_device_chained(falcon_ctx* ctx, int precision, const void* d_archive,
                                                const uint64_t* d_archive_bytes,
                                                const falcon_archive_info* info, void* d_values,
                                                uint64_t cap_values, void* stream);
+/* ---- batch index and random-access decode (the format itself has no batch
+ * index, FORMAT.md:10-14, so frames are otherwise located by a sequential walk) ---- */
+/* d_index (device, batch_count + 1 u64): index[b] = archive offset of batch b's frame
+ * (read_batch, container.cpp:113-132), index[batch_count] = end of the last frame.
+ * Synchronises `stream`; a malformed frame fails with the walker's message. */
+falcon_status falcon_archive_index(falcon_ctx* ctx, const void* d_archive, uint64_t archive_bytes,
+                                   const falcon_archive_info* info, uint64_t* d_index, void* stream);
+/* Decode batches [first_batch, first_batch + n_batches) only, given a HOST copy of the
+ * index: values first_batch * batch_values ... land at d_values[0 ...]; *n_values gets the
+ * count.  Same validation and messages as falcon_decompress_device (batch numbers absolute). */
+falcon_status falcon_decompress_device_range(falcon_ctx* ctx, int precision, const void* d_archive,
+                                             const falcon_archive_info* info, const uint64_t* index,
+                                             uint64_t first_batch, uint64_t n_batches, void* d_values,
+                                             uint64_t cap_values, uint64_t* n_values, void* stream);
 /* Profiling hook: when set (non-null), device-resident calls on ctx record enc_start /
  * enc_stop right before / after the encode kernel and dec_start / dec_stop around the
  * decode kernel, on the call's stream.  Pass nulls to clear. */

@@ -35,13 +35,14 @@ constexpr size_t kEncTicket = 0, kEncError = 8, kEncTotal = 16, kDecTicket = 24,
 
 uint8_t* misc_at(falcon_ctx* ctx, size_t off) { return ctx->misc.as<uint8_t>() + off; }
 
-falcon_status error_from_device(unsigned long long word, uint64_t cpb, bool batch_suffix) {
+falcon_status error_from_device(unsigned long long word, uint64_t cpb, bool batch_suffix,
+                                uint64_t first_batch = 0) {
     if (word == ~0ull) return FALCON_OK;
     const uint32_t code = (uint32_t)(word & 0xff);
     const uint64_t key = word >> 8;
     std::string msg = device_error_text(code);
     if (batch_suffix && code != DEV_E_TRAILING && code != DEV_E_CAPACITY && code != DEV_E_SCALE)
-        msg += " (batch " + std::to_string(key / cpb) + ")";
+        msg += " (batch " + std::to_string(first_batch + key / cpb) + ")";
     return set_error(device_error_status(code), msg);
 }
 
@@ -300,6 +301,66 @@ falcon_status falcon_decompress_device(falcon_ctx* ctx, int precision, const voi
     FB_TRY(error_from_device(err, g.cpb, true));
     if (n_values) *n_values = info.total_values;
     return FALCON_OK;
+}
+
+falcon_status falcon_archive_index(falcon_ctx* ctx, const void* d_archive, uint64_t archive_bytes,
+                                   const falcon_archive_info* info, uint64_t* d_index, void* stream) {
+    if (!ctx || !info || !d_index) return set_error(FALCON_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lock(ctx->api_mutex);
+    device_guard dg(ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    FB_CUDA(cudaMemsetAsync(misc_at(ctx, kDecError), 0xff, 8, st));
+    FB_CUDA(launch_index(static_cast<const uint8_t*>(d_archive), archive_bytes, 47, info->batch_count, d_index,
+                         reinterpret_cast<unsigned long long*>(misc_at(ctx, kDecError)), st));
+    uint8_t* hb = ctx->host_box.as<uint8_t>();
+    FB_CUDA(cudaMemcpyAsync(hb, misc_at(ctx, kDecError), 8, cudaMemcpyDeviceToHost, st));
+    FB_CUDA(cudaStreamSynchronize(st));
+    unsigned long long err;
+    std::memcpy(&err, hb, 8);
+    return error_from_device(err, 1, true);  // keys are batch numbers
+}
+
+falcon_status falcon_decompress_device_range(falcon_ctx* ctx, int precision, const void* d_archive,
+                                             const falcon_archive_info* info, const uint64_t* index,
+                                             uint64_t first_batch, uint64_t n_batches, void* d_values,
+                                             uint64_t cap_values, uint64_t* n_values, void* stream) {
+    if (!ctx || !info || !index) return set_error(FALCON_ERR_INVALID, "null argument");
+    if (first_batch > info->batch_count || n_batches > info->batch_count - first_batch)
+        return set_error(FALCON_ERR_INVALID, "batch range outside the archive");
+    if (info->precision != precision)
+        return set_error(FALCON_ERR_INVALID, "archive precision does not match the requested value type");
+    std::lock_guard<std::mutex> lock(ctx->api_mutex);
+    device_guard dg(ctx->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint64_t bv = info->batch_values;
+    const uint64_t v0 = first_batch * bv;
+    const uint64_t v1 = (first_batch + n_batches) * bv < info->total_values ? (first_batch + n_batches) * bv
+                                                                           : info->total_values;
+    const uint64_t count = n_batches ? v1 - v0 : 0;
+    if (count > cap_values) return set_error(FALCON_ERR_CAPACITY, "value capacity too small for the batch range");
+    if (n_values) *n_values = count;
+    if (count == 0) return FALCON_OK;
+    // the range's frames form a frames-only archive (no header) of `count` values
+    const uint64_t start = index[first_batch], end = index[first_batch + n_batches];
+    if (end < start) return set_error(FALCON_ERR_CORRUPT, "batch index is not increasing");
+    geometry g;
+    FB_TRY(make_geometry(count, info->chunk_n, bv, 0, g));
+    FB_TRY(ctx->dec_off.ensure(g.n_chunks * sizeof(uint64_t)));
+    FB_TRY(ctx->dec_size.ensure(g.n_chunks * sizeof(uint32_t)));
+    FB_TRY(ctx->dec_ready.ensure(g.n_batches * sizeof(uint32_t)));
+    FB_CUDA(cudaMemsetAsync(misc_at(ctx, kDecError), 0xff, 8, st));
+    const decode_ws ws = ctx_decode_ws(ctx);
+    const uint8_t* arc = static_cast<const uint8_t*>(d_archive) + start;
+    cudaError_t e = precision == FALCON_F64
+                        ? launch_decode<double>(arc, end - start, g, static_cast<double*>(d_values), ws, st)
+                        : launch_decode<float>(arc, end - start, g, static_cast<float*>(d_values), ws, st);
+    if (e != cudaSuccess) return set_error(FALCON_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
+    uint8_t* hb = ctx->host_box.as<uint8_t>();
+    FB_CUDA(cudaMemcpyAsync(hb, misc_at(ctx, kDecError), 8, cudaMemcpyDeviceToHost, st));
+    FB_CUDA(cudaStreamSynchronize(st));
+    unsigned long long err;
+    std::memcpy(&err, hb, 8);
+    return error_from_device(err, g.cpb, true, first_batch);
 }
 
 falcon_status falcon_ctx_set_kernel_events(falcon_ctx* ctx, void* enc_start, void* enc_stop,

@@ -698,6 +698,63 @@ __global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(con
     }
 }
 
+// Batch-offset index: one block walks the frames (read_batch,
+// container.cpp:113-132) and writes index[b] = archive offset of batch b's frame,
+// index[B] = end of the last frame.  Each size table is summed with independent
+// lane-contiguous loads, so a batch costs about one DRAM round trip.  A frame that does not fit the archive records
+// the same error codes as the decoder's walker.
+__global__ void __launch_bounds__(256) index_frames_kernel(const uint8_t* __restrict__ arc, uint64_t len,
+                                                           uint64_t header_bytes, uint64_t n_batches,
+                                                           uint64_t* __restrict__ index,
+                                                           unsigned long long* error) {
+    __shared__ uint32_t s_cnt, s_code;
+    __shared__ unsigned long long s_part[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint64_t cursor = header_bytes;
+    for (uint64_t b = 0; b < n_batches; ++b) {
+        if (tid == 0) {
+            index[b] = cursor;
+            s_code = 0;
+            if (len - cursor < 4) {
+                s_code = DEV_E_BATCH_HDR_TRUNC;
+            } else {
+                s_cnt = ld_u32_le(arc + cursor);
+                if (len - cursor < 4 + 4 * (uint64_t)s_cnt) s_code = DEV_E_TABLE_TRUNC;
+            }
+        }
+        __syncthreads();
+        if (s_code) {
+            if (tid == 0) record_error(error, b, s_code);
+            return;
+        }
+        const uint32_t cnt = s_cnt;
+        const uint64_t table = cursor + 4;
+        // sum of the u32 entries: lane-contiguous, independent loads (unrolled)
+        unsigned long long sum = 0;
+#pragma unroll 4
+        for (uint32_t i = tid; i < cnt; i += blockDim.x) sum += ld_u32_le(arc + table + 4 * (uint64_t)i);
+        for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
+        if (lane == 0) s_part[warp] = sum;
+        __syncthreads();
+        unsigned long long payload = 0;
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) payload += s_part[q];
+        const uint64_t next = table + 4 * (uint64_t)cnt;
+        if (len - next < payload) {
+            if (tid == 0) record_error(error, b, DEV_E_PAYLOAD_BATCH_TRUNC);
+            return;
+        }
+        cursor = next + payload;
+        __syncthreads();
+    }
+    if (tid == 0) index[n_batches] = cursor;
+}
+
+cudaError_t launch_index(const uint8_t* d_archive, uint64_t len, uint64_t header_bytes, uint64_t n_batches,
+                         uint64_t* d_index, unsigned long long* d_error, cudaStream_t st) {
+    index_frames_kernel<<<1, 256, 0, st>>>(d_archive, len, header_bytes, n_batches, d_index, d_error);
+    return cudaGetLastError();
+}
+
 template <typename T>
 uint32_t decode_smem_bytes(uint32_t chunk_n) {
     return kDecodeSlots * decode_region_bytes<T>(chunk_n);

@@ -59,6 +59,10 @@ cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry
                           const decode_ws& ws, cudaStream_t st, cudaEvent_t ev0 = nullptr,
                           cudaEvent_t ev1 = nullptr, const uint64_t* d_len = nullptr);
 
+// index[b] = archive offset of batch b's frame (b < n_batches), index[n_batches] = end
+cudaError_t launch_index(const uint8_t* d_archive, uint64_t len, uint64_t header_bytes, uint64_t n_batches,
+                         uint64_t* d_index, unsigned long long* d_error, cudaStream_t st);
+
 cudaError_t launch_selftest_dp(int prec, const void* v, uint64_t n, int A, int8_t* full,
                                int8_t* lit, int8_t* cert, int64_t* g, cudaStream_t st);
 

@@ -26,7 +26,7 @@ EXPORTED = [
     "falcon_ctx_destroy", "falcon_max_encoded_chunk_size", "falcon_compress_bound",
     "falcon_write_header", "falcon_read_header", "falcon_compress_device",
     "falcon_compress_device_async", "falcon_decompress_device", "falcon_decompress_device_async",
-    "falcon_decompress_device_chained",
+    "falcon_decompress_device_chained", "falcon_archive_index", "falcon_decompress_device_range",
     "falcon_ctx_sync", "falcon_compress_stream", "falcon_decompress_stream", "falcon_compress_host",
     "falcon_decompress_host", "falcon_compress_chunk", "falcon_decompress_chunk", "falcon_synth_fill",
     "falcon_ctx_set_kernel_events", "falcon_selftest_dp", "falcon_selftest_div",
@@ -105,6 +105,9 @@ def load() -> C.CDLL:
     L.falcon_decompress_device.argtypes = [vp, i32, vp, u64, vp, u64, C.POINTER(u64), vp]
     L.falcon_decompress_device_async.argtypes = [vp, i32, vp, u64, C.POINTER(ArchiveInfo), vp, u64, vp]
     L.falcon_decompress_device_chained.argtypes = [vp, i32, vp, vp, C.POINTER(ArchiveInfo), vp, u64, vp]
+    L.falcon_archive_index.argtypes = [vp, vp, u64, C.POINTER(ArchiveInfo), vp, vp]
+    L.falcon_decompress_device_range.argtypes = [vp, i32, vp, C.POINTER(ArchiveInfo), C.POINTER(u64), u64, u64,
+                                                 vp, u64, C.POINTER(u64), vp]
     L.falcon_ctx_sync.argtypes = [vp, vp]
     L.falcon_ctx_set_kernel_events.argtypes = [vp, vp, vp, vp, vp]
     L.falcon_selftest_dp.argtypes = [vp, i32, vp, u64, i32, vp, vp, vp, vp, vp]
@@ -250,6 +253,32 @@ class Codec:
             self.ctx, prec_of(out.dtype), C.c_void_p(archive.data_ptr()), C.c_void_p(nbytes_dev.data_ptr()),
             C.byref(info), C.c_void_p(out.data_ptr()), out.numel(), st))
         return out
+
+    def archive_index(self, archive, nbytes: int, stream=None):
+        """Batch-offset index of a device archive: numpy uint64[batch_count + 1]."""
+        import torch
+        info = read_header(archive[:47].cpu().numpy().tobytes())
+        idx = torch.empty(info.batch_count + 1, dtype=torch.int64, device=archive.device)
+        st = C.c_void_p(stream if stream is not None else torch.cuda.current_stream(archive.device).cuda_stream)
+        _check(self.lib.falcon_archive_index(self.ctx, C.c_void_p(archive.data_ptr()), nbytes, C.byref(info),
+                                             C.c_void_p(idx.data_ptr()), st))
+        return idx.cpu().numpy().view(np.uint64)
+
+    def decompress_range(self, archive, index, first_batch: int, n_batches: int, out=None, stream=None):
+        """Random-access decode of batches [first_batch, first_batch + n_batches)."""
+        import torch
+        info = read_header(archive[:47].cpu().numpy().tobytes())
+        dtype = torch.float64 if info.precision == F64 else torch.float32
+        if out is None:
+            out = torch.empty(max(n_batches * info.batch_values, 1), dtype=dtype, device=archive.device)
+        idx = np.ascontiguousarray(index, dtype=np.uint64)
+        nv = C.c_uint64()
+        st = C.c_void_p(stream if stream is not None else torch.cuda.current_stream(archive.device).cuda_stream)
+        _check(self.lib.falcon_decompress_device_range(
+            self.ctx, info.precision, C.c_void_p(archive.data_ptr()), C.byref(info),
+            idx.ctypes.data_as(C.POINTER(C.c_uint64)), first_batch, n_batches, C.c_void_p(out.data_ptr()),
+            out.numel(), C.byref(nv), st))
+        return out[: nv.value]
 
     def decompress_device_async(self, archive, nbytes: int, info: ArchiveInfo, out, stream=None):
         import torch
