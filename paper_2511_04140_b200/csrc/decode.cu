@@ -212,15 +212,12 @@ __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 
-#ifndef FB_DECODE_PRODUCERS
-#define FB_DECODE_PRODUCERS 2
-#endif
-#ifndef FB_DECODE_SLOTS
-#define FB_DECODE_SLOTS 4
-#endif
-constexpr int kDecodeSlots = FB_DECODE_SLOTS;   // smem ring depth (a multiple of kProducers:
-constexpr int kProducers = FB_DECODE_PRODUCERS; // each slot is refilled by one producer only)
-static_assert(kDecodeSlots % kProducers == 0, "slot reuse must stay within one producer");
+// Producer warps and smem ring depth per value type (A/B-measured on cfg2 / cfg3: 2 x 4
+// for both; 1 x 3, 2 x 6, 3 x 6, 3 x 9, 4 x 8 are slower or unstable).  The ring depth is a
+// multiple of the producer count: each slot is refilled by one producer only.
+template <typename T> struct decode_cfg { static constexpr int producers = 2, slots = 4; };
+static_assert(decode_cfg<double>::slots % decode_cfg<double>::producers == 0, "slot reuse");
+static_assert(decode_cfg<float>::slots % decode_cfg<float>::producers == 0, "slot reuse");
 enum : uint32_t { SLOT_CHUNK = 0, SLOT_SKIP = 1, SLOT_EXIT = 2 };
 
 // value staging for coalesced stores: [8][NT + 2] values (+ value 0), reusing the slot
@@ -380,11 +377,13 @@ __device__ __forceinline__ void parse_chunk(const uint8_t* p, const uint8_t* hp,
 // only gather, scan and store.  Staging and parsing of later chunks overlap the decode
 // of the current one; the next chunk's offsets are fetched while a copy is in flight.
 template <typename T, int NT>
-__global__ void __launch_bounds__(NT + 32 * kProducers) decode_chunks_kernel(const uint8_t* __restrict__ arc, uint64_t len_arg,
+__global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers) decode_chunks_kernel(const uint8_t* __restrict__ arc, uint64_t len_arg,
                                                                 const uint64_t* __restrict__ d_len,
                                                                 geometry g, T* __restrict__ out,
                                                                 decode_ws ws) {
     const uint64_t len = d_len ? *d_len : len_arg;
+    constexpr int kProducers = decode_cfg<T>::producers;
+    constexpr int kDecodeSlots = decode_cfg<T>::slots;
     using tr = lane_traits<T>;
     using B = typename tr::B;
     using S = typename tr::S;
@@ -757,7 +756,7 @@ cudaError_t launch_index(const uint8_t* d_archive, uint64_t len, uint64_t header
 
 template <typename T>
 uint32_t decode_smem_bytes(uint32_t chunk_n) {
-    return kDecodeSlots * decode_region_bytes<T>(chunk_n);
+    return decode_cfg<T>::slots * decode_region_bytes<T>(chunk_n);
 }
 
 template <typename T>
@@ -789,7 +788,7 @@ cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
     // persistent grid: every block co-resident (block 0 walks frames, the rest spin on it)
     int per_sm = 0, dev = 0, sms = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)threads + 32 * kProducers, smem))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)threads + 32 * decode_cfg<T>::producers, smem))) return e;
     if ((e = cudaGetDevice(&dev))) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev))) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
@@ -797,7 +796,7 @@ cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry
     if (grid > g.n_chunks + 1) grid = g.n_chunks + 1;
     if (grid < 2) grid = 2;
     if (ev0 && (e = cudaEventRecord(ev0, st))) return e;
-    kern<<<(unsigned)grid, threads + 32 * kProducers, smem, st>>>(d_archive, len, d_len, g, d_out, ws);
+    kern<<<(unsigned)grid, threads + 32 * decode_cfg<T>::producers, smem, st>>>(d_archive, len, d_len, g, d_out, ws);
     if ((e = cudaGetLastError())) return e;
     return ev1 ? cudaEventRecord(ev1, st) : cudaSuccess;
 }
