@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? FB_ENC_MIN_BLOCKS : (2048 / NT
     __shared__ uint32_t s_warpw[nwarps];
     __shared__ __align__(16) uint32_t s_rowoff[64];        // plane p: row offset in the image
     __shared__ uint32_t s_nzc[nwarps][16];   // 8-bit nonzero-byte counters, 4 planes/word
-    __shared__ __align__(16) uint16_t s_wpre[nwarps * 64]; // [w][p]: nonzero bytes of plane p in warps before w
+    __shared__ __align__(16) uint32_t s_pbase[nwarps * 64]; // [w][p]: payload position of warp w's first byte in row p
     __shared__ uint64_t s_dense;
     __shared__ uint32_t s_size;
     __shared__ B s_z1;
@@ -359,13 +359,14 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? FB_ENC_MIN_BLOCKS : (2048 / NT
     // ---- sizes and row offsets (warp 0): plane p is row w-1-p ----
     if (warp == 0) {
         uint32_t nz0 = 0, nz1 = 0;  // nonzero bytes of planes `lane` and `lane + 32`
+        uint32_t wp0[nwarps], wp1[nwarps];  // payload bytes of planes lane / lane+32 in warps before q
 #pragma unroll
         for (int q = 0; q < nwarps; ++q) {
             const int wq = (int)s_warpw[q];
             const uint32_t c0 = lane < wq ? (s_nzc[q][lane >> 2] >> (8 * (lane & 3))) & 0xffu : 0u;
             const uint32_t c1 = lane + 32 < wq ? (s_nzc[q][(lane + 32) >> 2] >> (8 * (lane & 3))) & 0xffu : 0u;
-            s_wpre[q * 64 + lane] = (uint16_t)nz0;
-            s_wpre[q * 64 + lane + 32] = (uint16_t)nz1;
+            wp0[q] = nz0;
+            wp1[q] = nz1;
             nz0 += c0;
             nz1 += c1;
         }
@@ -392,8 +393,15 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? FB_ENC_MIN_BLOCKS : (2048 / NT
         const uint32_t tot1 = __shfl_sync(0xffffffffu, s1, 0);
         const uint32_t tot0 = __shfl_sync(0xffffffffu, s0, 0);
         const uint32_t base = HDR + fb;
-        s_rowoff[lane + 32] = base + (s1 - c1);
-        s_rowoff[lane] = base + tot1 + (s0 - c0);
+        const uint32_t ro1 = base + (s1 - c1), ro0 = base + tot1 + (s0 - c0);
+        s_rowoff[lane + 32] = ro1;
+        s_rowoff[lane] = ro0;
+        // sparse payload start of plane p for warp q: row offset + bitmap + earlier warps
+#pragma unroll
+        for (int q = 0; q < nwarps; ++q) {
+            s_pbase[q * 64 + lane] = ro0 + (uint32_t)BM + wp0[q];
+            s_pbase[q * 64 + lane + 32] = ro1 + (uint32_t)BM + wp1[q];
+        }
         const uint32_t dm0 = __ballot_sync(0xffffffffu, d0);
         const uint32_t dm1 = __ballot_sync(0xffffffffu, d1);
         const uint32_t size = w ? base + tot1 + tot0 : (uint32_t)HDR;
@@ -462,9 +470,9 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? FB_ENC_MIN_BLOCKS : (2048 / NT
         // image byte below `size` is written (bitmaps always, payloads are contiguous), so
         // the staging buffer needs no zeroing.
         if (sblk) {
-            const uint4 wp = *reinterpret_cast<const uint4*>(&s_wpre[warp * 64 + 8 * sb]);
-            const uint32_t wpre[8] = {wp.x & 0xffffu, wp.x >> 16, wp.y & 0xffffu, wp.y >> 16,
-                                      wp.z & 0xffffu, wp.z >> 16, wp.w & 0xffffu, wp.w >> 16};
+            const uint4 pb03 = *reinterpret_cast<const uint4*>(&s_pbase[warp * 64 + 8 * sb]);
+            const uint4 pb47 = *reinterpret_cast<const uint4*>(&s_pbase[warp * 64 + 8 * sb + 4]);
+            const uint32_t pbase[8] = {pb03.x, pb03.y, pb03.z, pb03.w, pb47.x, pb47.y, pb47.z, pb47.w};
             uint32_t mk[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -482,7 +490,7 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? FB_ENC_MIN_BLOCKS : (2048 / NT
             for (int k = 0; k < 8; ++k) {
                 const uint32_t byte = (k < 4 ? ylo >> (8 * k) : yhi >> (8 * (k - 4))) & 0xffu;
                 if (((sblk >> k) & 1u) && byte != 0u)
-                    s_stage[off[k] + BM + wpre[k] + __popc(mk[k] & lt_mask)] = (uint8_t)byte;
+                    s_stage[pbase[k] + __popc(mk[k] & lt_mask)] = (uint8_t)byte;
             }
         }
     }
