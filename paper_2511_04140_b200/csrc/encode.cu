@@ -48,24 +48,8 @@ __device__ __forceinline__ uint32_t warp_or(uint32_t v) {
     return __reduce_or_sync(0xffffffffu, v);
 }
 
-template <typename B>
-__device__ __forceinline__ B warp_max(B v);
-template <>
-__device__ __forceinline__ uint64_t warp_max(uint64_t v) {
-    const uint32_t hi = __reduce_max_sync(0xffffffffu, (uint32_t)(v >> 32));
-    const uint32_t lo = __reduce_max_sync(0xffffffffu, (uint32_t)(v >> 32) == hi ? (uint32_t)v : 0u);
-    return ((uint64_t)hi << 32) | lo;
-}
-template <>
-__device__ __forceinline__ uint32_t warp_max(uint32_t v) {
-    return __reduce_max_sync(0xffffffffu, v);
-}
-
 __device__ __forceinline__ int bit_width(uint64_t x) { return x ? 64 - __clzll((long long)x) : 0; }
 __device__ __forceinline__ int bit_width(uint32_t x) { return x ? 32 - __clz((int)x) : 0; }
-
-__device__ __forceinline__ uint32_t byte_of(uint64_t x, int s) { return (uint32_t)(x >> (8 * s)) & 0xffu; }
-__device__ __forceinline__ uint32_t byte_of(uint32_t x, int s) { return (x >> (8 * s)) & 0xffu; }
 
 }  // namespace
 
@@ -77,21 +61,9 @@ __host__ __device__ __forceinline__ uint32_t encode_stage_bytes(uint32_t chunk_n
     return (uint32_t)(tr::header + (tr::width + 7) / 8 + tr::width * nc + 32 + 15) & ~15u;
 }
 
-// compile-time bound of encode_stage_bytes over the chunk sizes a CTA of NT threads serves
-template <typename T, int NT>
-__host__ __device__ constexpr uint32_t encode_stage_bytes_max() {
-    return (uint32_t)(lane_traits<T>::header + (lane_traits<T>::width + 7) / 8 + lane_traits<T>::width * NT + 32 + 15) & ~15u;
-}
-
 // 32-bit word of lane values whose byte q is gathered (sb < 4: low word, else high)
 __device__ __forceinline__ uint32_t lane_word(uint64_t z, int sb) { return sb < 4 ? (uint32_t)z : (uint32_t)(z >> 32); }
 __device__ __forceinline__ uint32_t lane_word(uint32_t z, int) { return z; }
-
-// st.shared.u8 under a predicate: no branch, no reconvergence block
-__device__ __forceinline__ void st_u8_if(bool p, uint8_t* addr, uint32_t v) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.u8 [%1], %2;\n\t}"
-                 ::"r"((uint32_t)p), "r"((uint32_t)__cvta_generic_to_shared(addr)), "r"(v) : "memory");
-}
 
 // 0x01 in every nonzero byte of w
 __device__ __forceinline__ uint32_t nonzero_bytes(uint32_t w) {

@@ -203,10 +203,6 @@ __device__ __forceinline__ void st_release32(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// padded smem index: one spare slot per 8 values keeps the byte-column reads
-// (thread t touching values 8t..8t+8) free of bank conflicts
-__host__ __device__ __forceinline__ uint32_t pidx(uint32_t i) { return i + (i >> 3); }
-
 __device__ __forceinline__ void record_error(unsigned long long* err, uint64_t key, uint32_t code) {
     atomicMin(err, (unsigned long long)((key << 8) | code));
 }
