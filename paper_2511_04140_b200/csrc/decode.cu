@@ -134,16 +134,16 @@ __device__ void walk_frames(const uint8_t* __restrict__ arc, uint64_t len, const
                 record_error(ws.error, first, code);
                 atomicMin(ws.abort_at, (unsigned long long)b);
             } else {
+                // the block's offset stores are ordered before this point by the barrier
+                // after the write loop; one fence + release publishes them (the usual
+                // single-writer pattern: barrier, fence, flag)
                 __threadfence();
+                st_release32(&ws.ready[b], 1u);
             }
             s_code = code;
         }
         __syncthreads();
         if (s_code) return;
-        // every thread's offset stores are ordered before the release by its own fence
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) st_release32(&ws.ready[b], 1u);
         cursor = pay0 + carry;
     }
     if (tid == 0 && cursor != len) record_error(ws.error, g.n_chunks, DEV_E_TRAILING);  // pipeline.hpp:460-461
