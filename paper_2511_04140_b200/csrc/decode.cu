@@ -35,13 +35,14 @@ __device__ __forceinline__ uint32_t ld_u32_le(const uint8_t* p) {
 // `cap` entries), scanned block-wide, and the chunk offsets/sizes are written back with
 // lane-contiguous stores, so one batch costs about one DRAM round trip plus the fence.
 __device__ void walk_frames(const uint8_t* __restrict__ arc, uint64_t len, const geometry& g,
-                            const decode_ws& ws, uint4* s_raw, uint32_t* s_pref, uint32_t cap) {
+                            const decode_ws& ws, uint4* s_raw, uint32_t* s_pref, uint32_t cap,
+                            uint64_t b0, uint64_t cursor0) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nthreads = blockDim.x, nwarps = nthreads >> 5;
     __shared__ uint32_t s_cnt, s_code;
     __shared__ uint32_t s_wsum[32];
-    uint64_t cursor = g.header_bytes;
-    for (uint64_t b = 0; b < g.n_batches; ++b) {
+    uint64_t cursor = cursor0;
+    for (uint64_t b = b0; b < g.n_batches; ++b) {
         const uint64_t first = b * g.cpb;
         if (tid == 0) {
             s_code = 0;
@@ -147,6 +148,113 @@ __device__ void walk_frames(const uint8_t* __restrict__ arc, uint64_t len, const
         cursor = pay0 + carry;
     }
     if (tid == 0 && cursor != len) record_error(ws.error, g.n_chunks, DEV_E_TRAILING);  // pipeline.hpp:460-461
+}
+
+
+// Fast path of the frame walk for the common case (16-B aligned archive, every table fits
+// the smem buffer): the next batch's count + size table are loaded into registers while
+// the current batch's offsets are written, so a batch costs about one DRAM round trip
+// less.  It stops, before writing anything for the batch, at the first frame that is not
+// exactly as expected (wrong count, truncation); the general walker then resumes there
+// and reports the reference's error.  Returns the first batch not published.
+template <int PF>
+__device__ uint64_t walk_frames_fast(const uint8_t* __restrict__ arc, uint64_t len, const geometry& g,
+                                     const decode_ws& ws, uint4* s_raw, uint32_t* s_pref, uint32_t cap,
+                                     uint64_t* cursor_out) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nthreads = blockDim.x, nwarps = nthreads >> 5;
+    __shared__ uint32_t s_wsum[32];
+    uint64_t cursor = g.header_bytes;
+    *cursor_out = cursor;
+    if ((((uintptr_t)arc) & 15) != 0 || (uint64_t)g.cpb + 8 > cap) return 0;
+    auto nvec_of = [&](uint64_t cur, uint32_t cnt) -> uint32_t {
+        return (uint32_t)(((cur & 15) + 4 + 4 * (uint64_t)cnt + 15) >> 4);
+    };
+    uint4 pf[PF];
+    auto issue = [&](uint64_t cur, uint32_t cnt) {
+        const uint64_t v0 = cur & ~15ull;
+        const uint32_t nvec = nvec_of(cur, cnt);
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            const uint32_t v = (uint32_t)tid + (uint32_t)k * nthreads;
+            pf[k] = make_uint4(0u, 0u, 0u, 0u);
+            if (v < nvec) {
+                const uint64_t at = v0 + 16ull * v;
+                if (at + 16 <= len) {
+                    pf[k] = __ldg(reinterpret_cast<const uint4*>(arc + at));
+                } else {
+                    uint32_t wv[4] = {0u, 0u, 0u, 0u};
+                    for (int q = 0; q < 16; ++q)
+                        if (at + q < len) wv[q >> 2] |= (uint32_t)arc[at + q] << (8 * (q & 3));
+                    pf[k] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                }
+            }
+        }
+    };
+    if (g.n_batches == 0) return 0;
+    if (nvec_of(cursor, g.chunks_in(0)) > (uint32_t)PF * nthreads) return 0;
+    issue(cursor, g.chunks_in(0));
+    uint64_t b = 0;
+    for (; b < g.n_batches; ++b) {
+        const uint32_t exp = g.chunks_in(b);
+        const uint32_t nvec = nvec_of(cursor, exp);
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            const uint32_t v = (uint32_t)tid + (uint32_t)k * nthreads;
+            if (v < nvec) s_raw[v] = pf[k];
+        }
+        __syncthreads();
+        const uint8_t* rb = reinterpret_cast<const uint8_t*>(s_raw) + (cursor & 15);
+        // stop (uniformly) at anything unusual: the general walker takes over
+        if (len - cursor < 4 + 4 * (uint64_t)exp || ld_u32_le(rb) != exp) break;
+        const uint8_t* tb = rb + 4;
+        auto entry = [&](uint32_t i) -> uint32_t { return ld_u32_le(tb + 4 * i); };
+        const uint32_t per = (exp + nthreads - 1) / nthreads;
+        const uint32_t i0 = min(exp, (uint32_t)tid * per), i1 = min(exp, i0 + per);
+        uint32_t mine = 0;
+        for (uint32_t i = i0; i < i1; ++i) mine += entry(i);
+        uint32_t incl = mine;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += t;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        uint32_t run = incl - mine, payload = 0;
+        for (int w = 0; w < nwarps; ++w) {
+            if (w < warp) run += s_wsum[w];
+            payload += s_wsum[w];
+        }
+        for (uint32_t i = i0; i < i1; ++i) {
+            s_pref[i] = run;
+            run += entry(i);
+        }
+        const uint64_t pay0 = cursor + 4 + 4 * (uint64_t)exp;
+        if (len - pay0 < payload) break;  // truncated payload: the general walker reports it
+        const uint64_t next = pay0 + payload;
+        const bool more = b + 1 < g.n_batches && nvec_of(next, g.chunks_in(b + 1)) <= (uint32_t)PF * nthreads;
+        if (more) issue(next, g.chunks_in(b + 1));  // in flight while this batch is written
+        __syncthreads();
+        const uint64_t first = b * g.cpb;
+        for (uint32_t i = tid; i < exp; i += nthreads) {
+            ws.chunk_off[first + i] = pay0 + s_pref[i];
+            ws.chunk_size[first + i] = entry(i);
+        }
+        __syncthreads();
+        if (tid == 0) {  // barrier, fence, flag (see walk_frames)
+            __threadfence();
+            st_release32(&ws.ready[b], 1u);
+        }
+        cursor = next;
+        *cursor_out = cursor;
+        if (!more) {
+            ++b;
+            break;
+        }
+    }
+    __syncthreads();
+    return b;
 }
 
 }  // namespace
@@ -366,8 +474,27 @@ __device__ __forceinline__ void parse_chunk(const uint8_t* p, const uint8_t* hp,
     }
 }
 
-// Persistent, warp-specialized decode.  Block 0 is the frame walker.  In every other
-// block the last kProducers warps are producers: each takes chunk tickets, waits for
+// The frame walker as its own one-block kernel, launched just before the decoder with
+// programmatic dependent launch: it lets the decoder start at once
+// (griddepcontrol.launch_dependents), and the decoder's producers wait on the per-batch
+// ready flags it publishes.  Its own register and smem budget keep the next batch's table
+// in flight without costing the decoder occupancy.
+constexpr int kWalkThreads = 512;
+__global__ void __launch_bounds__(kWalkThreads) walker_kernel(const uint8_t* __restrict__ arc, uint64_t len_arg,
+                                                              const uint64_t* __restrict__ d_len, geometry g,
+                                                              decode_ws ws, uint32_t cap) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint64_t len = d_len ? *d_len : len_arg;
+    extern __shared__ __align__(16) uint8_t wsmem[];
+    uint4* raw = reinterpret_cast<uint4*>(wsmem);                 // 4 cap + 32 bytes
+    uint32_t* pref = reinterpret_cast<uint32_t*>(wsmem + 4 * (size_t)cap + 32);  // cap entries
+    uint64_t cursor;
+    const uint64_t b0 = walk_frames_fast<4>(arc, len, g, ws, raw, pref, cap, &cursor);
+    walk_frames(arc, len, g, ws, raw, pref, cap, b0, cursor);
+}
+
+// Persistent, warp-specialized decode (the frame walker runs beside it, walker_kernel).
+// In every block the last kProducers warps are producers: each takes chunk tickets, waits for
 // the walker to publish its chunk's batch, streams the chunk bytes (16-B
 // cp.async at the source's 16-B phase) into a ring of kDecodeSlots smem slots, parses
 // and validates the staged chunk, and hands the slot to the NT consumer threads, which
@@ -393,13 +520,6 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers) decode_chu
     const int NC = (int)((n - 1) / 8);
     const int BM = NC / 8;  // sparse bitmap bytes (bitplane.hpp:113-122)
     const uint32_t region = decode_region_bytes<T>(n);
-    if (blockIdx.x == 0) {  // the slot ring of block 0 is the walker's table buffer
-        // raw table bytes (4 cap + 32) then cap prefixes
-        const uint32_t cap = ((kDecodeSlots * region) - 48) / 8 & ~3u;
-        walk_frames(arc, len, g, ws, reinterpret_cast<uint4*>(smem),
-                    reinterpret_cast<uint32_t*>(smem + 4 * cap + 32), cap);
-        return;
-    }
 
     __shared__ __align__(8) uint64_t s_full[kDecodeSlots], s_empty[kDecodeSlots];
     __shared__ SI s_info[kDecodeSlots];
@@ -783,18 +903,35 @@ cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry
     }
     if (!kern) return cudaErrorInvalidConfiguration;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-    // persistent grid: every block co-resident (block 0 walks frames, the rest spin on it)
+    // persistent grid, every block co-resident; the walker kernel goes first and lets the
+    // decoder launch immediately (programmatic dependent launch)
     int per_sm = 0, dev = 0, sms = 0;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)threads + 32 * decode_cfg<T>::producers, smem))) return e;
     if ((e = cudaGetDevice(&dev))) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev))) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     uint64_t grid = (uint64_t)per_sm * sms;
-    if (grid > g.n_chunks + 1) grid = g.n_chunks + 1;
-    if (grid < 2) grid = 2;
+    if (grid > g.n_chunks) grid = g.n_chunks;
+    if (grid < 1) grid = 1;
+    // walker smem: the whole size table of a batch when it fits (fast path), else segments
+    uint32_t cap = g.cpb + 64 < (24u << 10) ? g.cpb + 64 : (24u << 10);
+    cap = (cap + 3) & ~3u;
+    const size_t wsm = 8 * (size_t)cap + 48;
+    if ((e = cudaFuncSetAttribute(walker_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm))) return e;
     if (ev0 && (e = cudaEventRecord(ev0, st))) return e;
-    kern<<<(unsigned)grid, threads + 32 * decode_cfg<T>::producers, smem, st>>>(d_archive, len, d_len, g, d_out, ws);
+    walker_kernel<<<1, kWalkThreads, wsm, st>>>(d_archive, len, d_len, g, ws, cap);
     if ((e = cudaGetLastError())) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(threads + 32 * decode_cfg<T>::producers);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if ((e = cudaLaunchKernelEx(&cfg, kern, d_archive, len, d_len, g, d_out, ws))) return e;
     return ev1 ? cudaEventRecord(ev1, st) : cudaSuccess;
 }
 
