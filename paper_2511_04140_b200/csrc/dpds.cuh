@@ -281,10 +281,9 @@ template <> struct cert_params<double> {
 };
 template <> struct cert_params<float> {
     float p;
-    double pd;        // (double)p
     uint32_t lo;      // bits(dec(-A))
     uint32_t span;    // bits(dec(6 - A)) - bits(dec(-A))
-    uint32_t hk;      // hi(pd) - (151 << 20): hi word of H = p * 2^(ev - 24) is ((ab & EXP) >> 3) + hk
+    uint32_t hk;      // bits(p) - (151 << 23): bits of H = p * 2^(ev - 24) are (ab & EXP) + hk
 };
 
 __device__ __forceinline__ cert_params<double> cert_params_for(double, int A) {
@@ -302,10 +301,9 @@ __device__ __forceinline__ cert_params<float> cert_params_for(float, int A) {
     using X = fpx<float>;
     cert_params<float> c;
     c.p = X::pow10(A);
-    c.pd = (double)c.p;
     c.lo = X::dec(-A);
     c.span = X::dec(X::MAXB - A) - c.lo;
-    c.hk = (uint32_t)__double2hiint(c.pd) - (151u << 20);
+    c.hk = __float_as_uint(c.p) - (151u << 23);
     return c;
 }
 
@@ -330,10 +328,12 @@ __device__ __forceinline__ bool certify_lean(float v, const cert_params<float>& 
     const bool notpow2 = (ab & 0x007fffffu) != 0u;
     const float s = __fmul_rn(v, c.p);
     const float r = rintf(s);
-    const double e = __fma_rn(-(double)v, c.pd, (double)r);  // exact in double
-    const double H = __hiloint2double((int)(((ab & 0x7f800000u) >> 3) + c.hk), 0);
+    // e = r - v*p is a multiple of u = 2^(ev-23+A) (< 1/2 in range); whenever |e| < 2^24 u
+    // the FMA is exact, and H = 5^A u / 2 < 2^23 u (A <= 10), so |e| < H is decided exactly
+    const float e = __fmaf_rn(-v, c.p, r);
+    const float H = __uint_as_float((ab & 0x7f800000u) + c.hk);
     *g = (int32_t)__float2int_rz(r);
-    return inr && notpow2 && fabs(e) < H;
+    return inr && notpow2 && fabsf(e) < H;
 }
 
 // (3): decide v against candidate scale A (0 <= A <= max_alpha).  CERT_OK: alpha_v <= A
