@@ -356,7 +356,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": 4 * args.steps,   # encode, place, walker, decode
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
