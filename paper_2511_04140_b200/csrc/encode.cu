@@ -271,7 +271,8 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? FB_ENC_MIN_BLOCKS : (2048 / NT
             range_err |= !(fabs(s) < (T)0x1p62);  // numeric.hpp:153-154
             return (B)(S)llround_away(s);
         };
-        B gp = lane_g(vprev);
+        // (reuse: vprev is a chunk value with alpha_v <= A0, so rint is llround, as for gc)
+        B gp = reuse ? (B)(S)X::to_int(X::rint_(mul_rn(vprev, scale))) : lane_g(vprev);
         if (tid == 0) s_z1 = gp;
         if (reuse) {
 #pragma unroll
