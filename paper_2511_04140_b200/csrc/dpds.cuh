@@ -14,8 +14,8 @@
 //     the loop bounds (beta <= max_beta, so |s| < 10^15 for f64), e = N - v * 10^a is a
 //     multiple of 2^(ev-52+a) of magnitude < 2^53 of those units, so fma(-v, p, N)
 //     yields e exactly, and RN(N/p) == v  <=>  |e| < p * ulp(v)/2 (halved below a power
-//     of two), ties resolved to even -- all exact comparisons.  f32 uses a double
-//     residual (the 24x24-bit product is exact in double).
+//     of two), ties resolved to even -- all exact comparisons.  f32 keeps the residual
+//     in float: exact whenever |e| < 2^24 u (u its grid), while H < 2^23 u.
 // (3) Certification at a candidate scale A (alpha0 <= A <= loop bound).  If the
 //     reference test passes at some alpha_v <= A, then v*10^A lies within 3.5 ulp of
 //     N_v * 10^(A - alpha_v) and that integer is the N found at A (|s| < 2^50 makes the
@@ -77,14 +77,14 @@ template <> struct fpx<float> {
     __device__ static float rint_(float x) { return rintf(x); }
     __device__ static S to_int(float N) { return (S)__float2int_rz(N); }
     __device__ static bool recon_ok(float v, float p, float N) {
-        // residual in double: v*p (24 x 24 bits) is exact and N - v*p fits in 53 bits
-        const uint64_t eb = (uint64_t)__double_as_longlong(__fma_rn(-(double)v, (double)p, (double)N));
-        const uint64_t ae = eb & ~(1ull << 63);
+        // residual in float: a multiple of u = 2^(ev-23+a), exact whenever |e| < 2^24 u,
+        // while H = p * ulp(v) / 2 = 5^a u / 2 < 2^23 u (a <= 10): exact verdicts
+        const B eb = bits(__fmaf_rn(-v, p, N));
+        const B ae = eb & ~SIGN;
         const B vb = bits(v);
-        const uint64_t halve = (((eb >> 63) != (vb >> 31)) && (vb & MANT) == 0) ? 1 : 0;
-        // H = p * 2^(ev - 24) as a double
-        const uint64_t hb = (uint64_t)__double_as_longlong((double)p) +
-                            ((uint64_t)((vb >> MB) & EMASK) - (uint64_t)(BIAS + MB + 1) - halve << 52);
+        const B halve = (((eb ^ vb) & SIGN) != 0 && (vb & MANT) == 0) ? 1 : 0;
+        // H = p * 2^(ev - 24) (halved below a power of two) by exponent arithmetic
+        const B hb = bits(p) + (((vb >> MB) & EMASK) - (B)(BIAS + MB + 1) - halve << MB);
         return ae == 0 || ae < hb || (ae == hb && (vb & 1) == 0);
     }
 };
