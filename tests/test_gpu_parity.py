@@ -252,3 +252,15 @@ def test_chained_device_round_trip_without_host_sync(codec, oracle):
     assert int(d_nb.item()) == len(want)
     assert arc[: len(want)].cpu().numpy().tobytes() == want
     assert bits(back.cpu().numpy()) == bits(vals)
+
+
+@pytest.mark.parametrize("shift", [1, 3, 8, 13])
+def test_decode_from_unaligned_archive(codec, oracle, shift):
+    # the archive need not start on a 16-B boundary: staging, the frame walker and the
+    # vector loads all fall back to byte-exact paths
+    vals = synth("outlier", 3 * 1025 * 8 + 77, F64, dp=2, seed=9, period=100)
+    arc = oracle.compress_archive(vals, 1025, 1025 * 8)
+    buf = torch.zeros(len(arc) + 16, dtype=torch.uint8, device="cuda")
+    buf[shift:shift + len(arc)] = torch.frombuffer(bytearray(arc), dtype=torch.uint8).cuda()
+    back = codec.decompress_device(buf[shift:shift + len(arc)], len(arc)).cpu().numpy()
+    assert bits(back) == bits(vals)
