@@ -133,3 +133,14 @@ def test_deltas_crossing_the_32_bit_path(codec, oracle):
     sign = np.where(rng.integers(0, 2, len(base)) == 1, -1.0, 1.0)
     v = base * sign / 100.0
     check(codec, oracle, v)
+
+
+@pytest.mark.parametrize("step", [2 ** 22 - 1, -(2 ** 22), 2 ** 22, -(2 ** 22) - 1])
+def test_warp_scan_width_boundary(codec, oracle, step):
+    # constant deltas: zigzag width 23 for the first two steps (the decoder's 32-bit warp
+    # scan, warp sums reaching +-2^30), 24 for the others (64-bit scan)
+    rng = np.random.default_rng(9)
+    g = np.cumsum(np.full(16 * N, step, np.int64)) + int(rng.integers(-1000, 1000))
+    v = g.astype(np.float64)
+    v[N::2 * N] = -v[N::2 * N]     # odd chunks: a wide first delta (w = 35, 64-bit scan)
+    check(codec, oracle, v)
