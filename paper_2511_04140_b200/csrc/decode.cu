@@ -807,10 +807,17 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers) decode_chu
         // NT is a multiple of 8, so k % 8 is fixed per thread and k / 8 steps by NT / 8
         const int kb = tid - 1;
         const T* vsrc = vstage + (kb & 7) * (int)SP + (kb >> 3);
+        if (sizeof(T) == 8 && count == 8u * NT + 1u) {  // full f64 chunk (uniform): no bounds checks
 #pragma unroll
-        for (uint32_t m = 0; m < 9; ++m) {
-            const uint32_t i = (uint32_t)tid + NT * m;
-            if (m * NT < 8u * NT + 1u && i < count) dst[i] = i == 0 ? vstage[8 * SP] : vsrc[(NT / 8) * m];
+            for (uint32_t m = 0; m < 8; ++m)
+                dst[tid + NT * m] = (m == 0 && tid == 0) ? vstage[8 * SP] : vsrc[(NT / 8) * m];
+            if (tid == 0) dst[8 * NT] = vsrc[NT];
+        } else {
+#pragma unroll
+            for (uint32_t m = 0; m < 9; ++m) {
+                const uint32_t i = (uint32_t)tid + NT * m;
+                if (m * NT < 8u * NT + 1u && i < count) dst[i] = i == 0 ? vstage[8 * SP] : vsrc[(NT / 8) * m];
+            }
         }
     }
         }
