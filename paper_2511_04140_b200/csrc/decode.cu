@@ -315,6 +315,11 @@ __device__ __forceinline__ void consumer_sync() {
 // for both; 1 x 3, 2 x 6, 3 x 6, 3 x 9, 4 x 8 are slower or unstable).  The ring depth is a
 // multiple of the producer count: each slot is refilled by one producer only.
 template <typename T> struct decode_cfg { static constexpr int producers = 2, slots = 4; };
+// f32 at the default chunk size: 6 resident blocks of 192 threads (56 registers; A/B vs no
+// bound -3 %, vs 7 / 8 blocks, which spill, -2 % / -1 %).  f64 (0 = no bound) allocates 56
+// registers by itself; the slot ring allows 6 f64 blocks per SM anyway.
+template <typename T, int NT>
+constexpr int decode_min_blocks() { return sizeof(T) == 4 && NT <= 128 ? 6 : 0; }
 static_assert(decode_cfg<double>::slots % decode_cfg<double>::producers == 0, "slot reuse");
 static_assert(decode_cfg<float>::slots % decode_cfg<float>::producers == 0, "slot reuse");
 enum : uint32_t { SLOT_CHUNK = 0, SLOT_SKIP = 1, SLOT_EXIT = 2 };
@@ -495,7 +500,7 @@ __global__ void __launch_bounds__(kWalkThreads) walker_kernel(const uint8_t* __r
 // only gather, scan and store.  Staging and parsing of later chunks overlap the decode
 // of the current one; the next chunk's offsets are fetched while a copy is in flight.
 template <typename T, int NT>
-__global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers) decode_chunks_kernel(const uint8_t* __restrict__ arc, uint64_t len_arg,
+__global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers, decode_min_blocks<T, NT>()) decode_chunks_kernel(const uint8_t* __restrict__ arc, uint64_t len_arg,
                                                                 const uint64_t* __restrict__ d_len,
                                                                 geometry g, T* __restrict__ out,
                                                                 decode_ws ws) {
