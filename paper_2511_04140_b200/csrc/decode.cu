@@ -315,8 +315,9 @@ __device__ __forceinline__ void consumer_sync() {
 // for both; 1 x 3, 2 x 6, 3 x 6, 3 x 9, 4 x 8 are slower or unstable).  The ring depth is a
 // multiple of the producer count: each slot is refilled by one producer only.
 template <typename T> struct decode_cfg { static constexpr int producers = 2, slots = 4; };
-// f32 at the default chunk size: 6 resident blocks of 192 threads (56 registers; A/B vs no
-// bound -3 %, vs 7 / 8 blocks, which spill, -2 % / -1 %).  f64 (0 = no bound) allocates 56
+// f32 at the default chunk size: 6 resident blocks of 192 threads (56 registers; A/B: vs no
+// bound -0.3 %, vs a 1-block bound (62 registers, 5 blocks) -3 %, vs 7 / 8 blocks, which
+// spill, -2 % / -1 %).  f64 (0 = no bound) allocates 56
 // registers by itself; the slot ring allows 6 f64 blocks per SM anyway.
 template <typename T, int NT>
 constexpr int decode_min_blocks() { return sizeof(T) == 4 && NT <= 128 ? 6 : 0; }
