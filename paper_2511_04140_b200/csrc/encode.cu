@@ -70,11 +70,22 @@ __device__ __forceinline__ uint32_t nonzero_bytes(uint32_t w) {
     return ((((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w) >> 7) & 0x01010101u;
 }
 
+// resident CTAs of <= 128 threads per SM the register budget targets.  The encoder is
+// latency-bound between its block barriers, so occupancy pays until spills dominate:
+// f64 at 8 (64 registers; 6 / 7 / 9 / 10 blocks are slower), f32 at 16 (32 registers;
+// cfg3 encode 1.65 ms at 8 blocks, 1.39 ms at 12, 1.35 ms at 16)
 #ifndef FB_ENC_MIN_BLOCKS
-#define FB_ENC_MIN_BLOCKS 8   // resident CTAs of 128 threads per SM the register budget targets
+#define FB_ENC_MIN_BLOCKS 8
+#endif
+#ifndef FB_ENC_MIN_BLOCKS32
+#define FB_ENC_MIN_BLOCKS32 16
 #endif
 template <typename T, int NT>
-__global__ void __launch_bounds__(NT, NT <= 128 ? FB_ENC_MIN_BLOCKS : (2048 / NT > 0 ? 2048 / NT : 1))
+constexpr int encode_min_blocks() {
+    return NT <= 128 ? (sizeof(T) == 4 ? FB_ENC_MIN_BLOCKS32 : FB_ENC_MIN_BLOCKS) : (2048 / NT > 0 ? 2048 / NT : 1);
+}
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     encode_chunks_kernel(const T* __restrict__ in, geometry g, uint8_t* __restrict__ out,
                          uint64_t out_cap, encode_ws ws) {
     using tr = lane_traits<T>;
