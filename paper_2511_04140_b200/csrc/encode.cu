@@ -72,10 +72,11 @@ __device__ __forceinline__ uint32_t nonzero_bytes(uint32_t w) {
 
 // resident CTAs of <= 128 threads per SM the register budget targets.  The encoder is
 // latency-bound between its block barriers, so occupancy pays until spills dominate:
-// f64 at 8 (64 registers; 6 / 7 / 9 / 10 blocks are slower), f32 at 16 (32 registers;
-// cfg3 encode 1.65 ms at 8 blocks, 1.39 ms at 12, 1.35 ms at 16)
+// f64 at 9 (56 registers, no spills; cfg2 encode 1.139 ms at 8 blocks, 1.106 ms at 9,
+// 1.143 ms at 10 with spills), f32 at 16 (32 registers; cfg3 encode 1.65 ms at 8 blocks,
+// 1.39 ms at 12, 1.35 ms at 16)
 #ifndef FB_ENC_MIN_BLOCKS
-#define FB_ENC_MIN_BLOCKS 8
+#define FB_ENC_MIN_BLOCKS 9
 #endif
 #ifndef FB_ENC_MIN_BLOCKS32
 #define FB_ENC_MIN_BLOCKS32 16
@@ -165,7 +166,9 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     // ---- analyze, phase 2: lean certification of every value at A0 (dpds.cuh); the
     //      undecided ones (zeros, powers of two, decade edges, exceptions, alpha > A0)
     //      run the exact loop.  Thread 0 also covers value 0 (bit 8). ----
-    S gc[8];
+    // low words of the certified lane integers (all the 32-bit delta path needs; keeping
+    // 8 registers fewer lets 9 CTAs per SM run without spills)
+    uint32_t gc[8];
     uint32_t redo = 0;   // values the exact loop decides
     uint32_t f2 = 0;     // exception bit | one-hot alphas of values decided by the exact loop
     uint32_t mx = 0;     // max |v| high word (f32: bits) -> floor_log10(max|v|) for beta_hat
@@ -174,7 +177,9 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             uint32_t ah;
-            const bool ok = certify_lean(v[j], cp, &gc[j], &ah);
+            S g;
+            const bool ok = certify_lean(v[j], cp, &g, &ah);
+            gc[j] = (uint32_t)g;
             mx = ah > mx ? ah : mx;
             redo |= ok ? 0u : (1u << j);
         }
@@ -288,7 +293,9 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
         if (reuse) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                const B gj = (B)gc[j];
+                // f64: recompute certify's integer (only wide-integer chunks get here)
+                const B gj = sizeof(B) == 8 ? (B)(S)X::to_int(X::rint_(mul_rn(v[j], scale)))
+                                            : (B)(S)(int32_t)gc[j];
                 z[j] = zigzag<B>((B)(gj - gp));
                 gp = gj;
             }
