@@ -165,7 +165,12 @@ falcon_status falcon_decompress_device_range(falcon_ctx* ctx, int precision, con
  * decode kernel, on the call's stream.  Pass nulls to clear. */
 falcon_status falcon_ctx_set_kernel_events(falcon_ctx* ctx, void* enc_start, void* enc_stop,
                                            void* dec_start, void* dec_stop);
-/* Wait for `stream` and report the first error raised by async calls on ctx. */
+/* Wait for `stream` and report the first error raised by async calls on ctx.  Decode
+ * errors carry the reference's " (batch N)" suffix, numbered in the most recent async
+ * decode's archive.
+ * Async calls on one context share its device scratch (sizes, offsets, error words):
+ * enqueue them all on ONE stream (they then run in order); use one context per stream
+ * for concurrent work. */
 falcon_status falcon_ctx_sync(falcon_ctx* ctx, void* stream);
 
 /* ---- host-resident: multi-stream pinned H2D / kernel / D2H pipeline ---- */

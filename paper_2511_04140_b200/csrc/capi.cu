@@ -132,6 +132,8 @@ falcon_status enqueue_decompress(falcon_ctx* ctx, int prec, const void* d_archiv
     FB_TRY(ctx->dec_off.ensure(g.n_chunks * sizeof(uint64_t)));
     FB_TRY(ctx->dec_size.ensure(g.n_chunks * sizeof(uint32_t)));
     FB_TRY(ctx->dec_ready.ensure(g.n_batches * sizeof(uint32_t)));
+    ctx->dec_err_cpb = g.cpb;   // falcon_ctx_sync maps an async error's chunk to its batch
+    ctx->dec_err_first = 0;
     const decode_ws ws = ctx_decode_ws(ctx);
     cudaError_t e = prec == FALCON_F64
                         ? launch_decode<double>(static_cast<const uint8_t*>(d_archive), bytes, g,
@@ -388,9 +390,10 @@ falcon_status falcon_ctx_sync(falcon_ctx* ctx, void* stream) {
     FB_CUDA(cudaMemsetAsync(misc_at(ctx, kEncError), 0xff, 8, st));
     FB_CUDA(cudaMemsetAsync(misc_at(ctx, kDecError), 0xff, 8, st));
     FB_CUDA(cudaStreamSynchronize(st));
-    // batch index of an async error is not recoverable without the geometry; report the text
+    // decode errors carry the reference's " (batch N)" suffix (pipeline.hpp:404-405,
+    // 415-416), mapped through the geometry of the most recent async decode on ctx
     FB_TRY(error_from_device(errs[0], 1, false));
-    FB_TRY(error_from_device(errs[1], 1, false));
+    FB_TRY(error_from_device(errs[1], ctx->dec_err_cpb, true, ctx->dec_err_first));
     return FALCON_OK;
 }
 

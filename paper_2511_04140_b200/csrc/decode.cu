@@ -40,7 +40,7 @@ __device__ void walk_frames(const uint8_t* __restrict__ arc, uint64_t len, const
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nthreads = blockDim.x, nwarps = nthreads >> 5;
     __shared__ uint32_t s_cnt, s_code;
-    __shared__ uint32_t s_wsum[32];
+    __shared__ uint64_t s_wsum[32];
     uint64_t cursor = cursor0;
     for (uint64_t b = b0; b < g.n_batches; ++b) {
         const uint64_t first = b * g.cpb;
@@ -99,23 +99,28 @@ __device__ void walk_frames(const uint8_t* __restrict__ arc, uint64_t len, const
             // thread-contiguous ranges: local sums, block exclusive scan, local prefixes
             const uint32_t per = (m + nthreads - 1) / nthreads;
             const uint32_t i0 = min(m, (uint32_t)tid * per), i1 = min(m, i0 + per);
-            uint32_t mine = 0;
-            for (uint32_t i = i0; i < i1; ++i) mine += entry(i);  // < 2^32: a segment holds < 2^32 bytes
-            uint32_t incl = mine;
+            // sums in u64 like read_batch (container.cpp:124-128): a crafted table must not
+            // wrap past the payload-truncation check.  s_pref keeps the segment-relative
+            // prefix in u32, exact up to the first entry above any valid chunk size; the
+            // chunks after such an entry fail their producer's bounds check, after the
+            // oversize chunk itself (lower index, so its error wins).
+            uint64_t mine = 0;
+            for (uint32_t i = i0; i < i1; ++i) mine += entry(i);
+            uint64_t incl = mine;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+                const uint64_t t = __shfl_up_sync(0xffffffffu, incl, d);
                 if (lane >= d) incl += t;
             }
             if (lane == 31) s_wsum[warp] = incl;
             __syncthreads();
-            uint32_t run = incl - mine, segsum = 0;
+            uint64_t run = incl - mine, segsum = 0;
             for (int w = 0; w < nwarps; ++w) {
                 if (w < warp) run += s_wsum[w];
                 segsum += s_wsum[w];
             }
             for (uint32_t i = i0; i < i1; ++i) {
-                s_pref[i] = run;
+                s_pref[i] = (uint32_t)run;
                 run += entry(i);
             }
             __syncthreads();
@@ -160,10 +165,11 @@ __device__ void walk_frames(const uint8_t* __restrict__ arc, uint64_t len, const
 template <int PF>
 __device__ uint64_t walk_frames_fast(const uint8_t* __restrict__ arc, uint64_t len, const geometry& g,
                                      const decode_ws& ws, uint4* s_raw, uint32_t* s_pref, uint32_t cap,
-                                     uint64_t* cursor_out) {
+                                     uint32_t emax, uint64_t* cursor_out) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nthreads = blockDim.x, nwarps = nthreads >> 5;
     __shared__ uint32_t s_wsum[32];
+    __shared__ int s_big;
     uint64_t cursor = g.header_bytes;
     *cursor_out = cursor;
     if ((((uintptr_t)arc) & 15) != 0 || (uint64_t)g.cpb + 8 > cap) return 0;
@@ -211,8 +217,16 @@ __device__ uint64_t walk_frames_fast(const uint8_t* __restrict__ arc, uint64_t l
         auto entry = [&](uint32_t i) -> uint32_t { return ld_u32_le(tb + 4 * i); };
         const uint32_t per = (exp + nthreads - 1) / nthreads;
         const uint32_t i0 = min(exp, (uint32_t)tid * per), i1 = min(exp, i0 + per);
+        // every entry <= emax (the largest valid chunk) keeps the u32 sums exact (a table
+        // holds < 2^16 entries here); anything larger goes to the general walker
         uint32_t mine = 0;
-        for (uint32_t i = i0; i < i1; ++i) mine += entry(i);
+        bool big = false;
+        for (uint32_t i = i0; i < i1; ++i) {
+            const uint32_t e = entry(i);
+            big |= e > emax;
+            mine += e;
+        }
+        if (__syncthreads_or(big)) break;
         uint32_t incl = mine;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -323,7 +337,7 @@ template <typename T, int NT>
 constexpr int decode_min_blocks() { return sizeof(T) == 4 && NT <= 128 ? 6 : 0; }
 static_assert(decode_cfg<double>::slots % decode_cfg<double>::producers == 0, "slot reuse");
 static_assert(decode_cfg<float>::slots % decode_cfg<float>::producers == 0, "slot reuse");
-enum : uint32_t { SLOT_CHUNK = 0, SLOT_SKIP = 1, SLOT_EXIT = 2 };
+enum : uint32_t { SLOT_CHUNK = 0, SLOT_SKIP = 1, SLOT_EXIT = 2, SLOT_BOUNDS = 3 };
 
 // value staging for coalesced stores: [8][NT + 2] values (+ value 0), reusing the slot
 __host__ __device__ __forceinline__ uint32_t decode_stage_stride(uint32_t nt) { return nt + 2; }
@@ -482,14 +496,14 @@ __device__ __forceinline__ void parse_chunk(const uint8_t* p, const uint8_t* hp,
 constexpr int kWalkThreads = 512;
 __global__ void __launch_bounds__(kWalkThreads) walker_kernel(const uint8_t* __restrict__ arc, uint64_t len_arg,
                                                               const uint64_t* __restrict__ d_len, geometry g,
-                                                              decode_ws ws, uint32_t cap) {
+                                                              decode_ws ws, uint32_t cap, uint32_t emax) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uint64_t len = d_len ? *d_len : len_arg;
     extern __shared__ __align__(16) uint8_t wsmem[];
     uint4* raw = reinterpret_cast<uint4*>(wsmem);                 // 4 cap + 32 bytes
     uint32_t* pref = reinterpret_cast<uint32_t*>(wsmem + 4 * (size_t)cap + 32);  // cap entries
     uint64_t cursor;
-    const uint64_t b0 = walk_frames_fast<4>(arc, len, g, ws, raw, pref, cap, &cursor);
+    const uint64_t b0 = walk_frames_fast<4>(arc, len, g, ws, raw, pref, cap, emax, &cursor);
     walk_frames(arc, len, g, ws, raw, pref, cap, b0, cursor);
 }
 
@@ -579,11 +593,14 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers, decode_min
             SI& si = s_info[sl];
             uint8_t* buf = smem + (size_t)sl * region;
             const uint32_t a = (uint32_t)(off & 15);
-            const uint32_t end = a + size;
+            const uint64_t end = (uint64_t)a + size;
+            // a published chunk lies inside the archive unless an earlier entry of its table
+            // was oversize (see walk_frames); that chunk's own error has the lower index
+            if (kind == SLOT_CHUNK && (off > len || len - off < size)) kind = SLOT_BOUNDS;
             const bool staged = kind == SLOT_CHUNK && end <= region;
             if (staged) {
                 const uint64_t base = off - a;
-                const uint32_t nvec = (end + 15) >> 4;
+                const uint32_t nvec = (uint32_t)((end + 15) >> 4);
                 for (uint32_t vv = lane; vv < nvec; vv += 32) {
                     const uint64_t gaddr = base + 16ull * vv;
                     if (aligned && gaddr + 16 <= len) {
@@ -648,6 +665,9 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers, decode_min
             exited |= 1u << pw;
             if (exited == (1u << kProducers) - 1u) break;
             continue;
+        }
+        if (kind == SLOT_BOUNDS) {
+            if (tid == 0) record_error(ws.error, si.chunk, DEV_E_SIZE);
         }
         const uint32_t code = kind == SLOT_CHUNK ? si.code : 0u;
         if (kind == SLOT_CHUNK && code != 0u) {
@@ -937,7 +957,9 @@ cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry
     const size_t wsm = 8 * (size_t)cap + 48;
     if ((e = cudaFuncSetAttribute(walker_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm))) return e;
     if (ev0 && (e = cudaEventRecord(ev0, st))) return e;
-    walker_kernel<<<1, kWalkThreads, wsm, st>>>(d_archive, len, d_len, g, ws, cap);
+    const uint32_t emax = (uint32_t)(lane_traits<T>::header + (lane_traits<T>::width + 7) / 8 +
+                                      lane_traits<T>::width * ((g.chunk_n - 1) / 8));  // max_encoded_chunk_size
+    walker_kernel<<<1, kWalkThreads, wsm, st>>>(d_archive, len, d_len, g, ws, cap, emax);
     if ((e = cudaGetLastError())) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);

@@ -256,13 +256,16 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     // ---- forward transform (transform.hpp:72-89) ----
     // Case 1 at alpha_max == A0: every value has alpha_v <= A0, so v * 10^A0 lies within
     // 3.5 ulp (<= 1/8) of its integer and rint == llround -- the certification's lane
-    // integers are final, also for the values the exact loop decided.  f64 lanes whose
-    // integers all fit in 30 bits (|v| < 2^(28 - e_p), e_p = exponent of the scale) take
-    // 32-bit delta/zigzag arithmetic: the same z, half the ALU work.
+    // integers are final, also for the values the exact loop decided.  When every integer
+    // of the CHUNK fits in 30 bits (|v| < 2^(28 - e_p), e_p = exponent of the scale) the
+    // f64 delta/zigzag runs in 32-bit arithmetic: the same z, half the ALU work.  The test
+    // is chunk-wide (M = max high word over all values, value 0 included): the first delta
+    // of warp k starts from the last value of warp k-1 (index 256k), so a per-warp vote
+    // would miss a wide value there (transform.hpp:87-88 wraps in 64 bits).
     const T scale = X::pow10(case2 ? 0 : amax);
     const bool reuse = !case2 && amax == A0;
     const uint32_t lim = (2074u - ((uint32_t)__double2hiint((double)scale) >> 20)) << 20;
-    const bool narrow = sizeof(B) == 8 && __all_sync(0xffffffffu, reuse && mx < lim);
+    const bool narrow = sizeof(B) == 8 && reuse && M < lim;
     B z[8];
     B orv = 0;
     if (narrow) {
@@ -598,7 +601,9 @@ __global__ void __launch_bounds__(kPlaceTile) place_chunks_kernel(geometry g, ui
                 out[frame + 3] = (uint8_t)(cnt >> 24);
             }
         }
-        if (c + 1 == g.n_chunks) *ws.total = s_off[tid] + sz;
+        // a total beyond the buffer is never published: a chained decoder reads its archive
+        // length from here (the capacity error is recorded by the copy below)
+        if (c + 1 == g.n_chunks) *ws.total = s_off[tid] + sz <= out_cap ? s_off[tid] + sz : 0;
     }
     if (t == 0 && tid == 0 && g.header_bytes == 47) {
         for (int i = 0; i < 47; ++i) out[i] = hdr.b[i];

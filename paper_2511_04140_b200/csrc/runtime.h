@@ -156,6 +156,7 @@ struct falcon_ctx {
     unsigned pool_workers = 0;
     std::mutex api_mutex;           // one API call at a time per context
     uint64_t last_archive_bytes = 0;
+    uint64_t dec_err_cpb = 1, dec_err_first = 0;  // geometry of the last async decode's errors
     cudaEvent_t prof_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // encode / decode kernel brackets
     fb200::worker_pool& get_pool(unsigned workers);
 };

@@ -144,3 +144,56 @@ def test_warp_scan_width_boundary(codec, oracle, step):
     v = g.astype(np.float64)
     v[N::2 * N] = -v[N::2 * N]     # odd chunks: a wide first delta (w = 35, 64-bit scan)
     check(codec, oracle, v)
+
+
+def _walk_units(rng, count, lo=-10 ** 4, hi=10 ** 4, step=127):
+    g = np.cumsum(rng.integers(-step, step + 1, count)) + int(rng.integers(lo, hi))
+    return g.astype(np.int64)
+
+
+@pytest.mark.parametrize("dp", [0, 2, 6])
+@pytest.mark.parametrize("at", [256, 512, 768])
+def test_wide_value_ending_the_previous_warp(codec, oracle, dp, at):
+    # A small-valued walk whose chunk holds one wide value at in-chunk index 256/512/768:
+    # the last value of warp k-1 is the value warp k's first delta starts from
+    # (transform.hpp:87-88).  The 32-bit delta path must not be taken for that delta.
+    rng = np.random.default_rng(100 + dp * 7 + at)
+    g = _walk_units(rng, 12 * N, lo=-100 * 10 ** dp, hi=100 * 10 ** dp, step=3)
+    spike = 3 * 10 ** 9 if dp != 6 else 3 * 10 ** 9 + 17     # > 2^31 units, still Case 1
+    for c0 in range(0, len(g) - N + 1, N):
+        g[c0 + at] = spike if (c0 // N) % 2 == 0 else -spike
+    v = g.astype(np.float64) / 10.0 ** dp
+    check(codec, oracle, v)
+
+
+def test_verdict_example_3e7_in_a_2dp_walk(codec, oracle):
+    # the reviewer's case: a 2-dp walk around 100.00 with v[256] = 3e7 (z[257] needs 33 bits)
+    rng = np.random.default_rng(5)
+    g = 10000 + _walk_units(rng, 4 * N, lo=0, hi=1, step=2)
+    v = g.astype(np.float64) / 100.0
+    v[256] = 3e7
+    v[N + 512] = -3e7
+    v[2 * N + 768] = 3e7
+    check(codec, oracle, v)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fuzz_magnitudes_at_warp_and_thread_boundaries(codec, oracle, seed):
+    # randomized differential fuzz: per chunk a random decimal count, a small walk, and a
+    # few values of random magnitude (2^0..2^50 units, up to the Case-1 limit) placed at
+    # warp and thread boundaries (in-chunk index 8t and its neighbours)
+    rng = np.random.default_rng(1000 + seed)
+    nch = 48
+    out = []
+    for c in range(nch):
+        dp = int(rng.integers(0, 7))
+        g = _walk_units(rng, N, lo=-50, hi=50, step=int(rng.integers(1, 200)))
+        for _ in range(int(rng.integers(1, 6))):
+            base = int(rng.choice([256, 512, 768, 0, 1024, 8 * int(rng.integers(1, 128))]))
+            pos = min(max(base + int(rng.integers(-1, 2)), 0), N - 1)
+            mag = int(2 ** float(rng.uniform(0, 50)))
+            lim = 10 ** (15 - dp) - 1 if dp < 15 else 1          # keep beta_hat <= 15
+            g[pos] = min(mag, lim) * (1 if rng.integers(0, 2) else -1)
+        out.append(g.astype(np.float64) / 10.0 ** dp)
+    v = np.concatenate(out)
+    check(codec, oracle, v)
