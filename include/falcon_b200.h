@@ -224,6 +224,10 @@ falcon_status falcon_selftest_div(falcon_ctx* ctx, int precision, const int64_t*
 #define FALCON_KIND_OUTLIER 3
 #define FALCON_KIND_BITS 4
 #define FALCON_KIND_MIXED_BLOCKS 5
+/* Counter-based "HPC field" for the sharded configs (not a reference kind; pinned in
+ * csrc/field.cuh and restated in oracle/): value i depends on (seed, i) only, so any
+ * range is produced directly, on the host or on the device. */
+#define FALCON_KIND_FIELD 6
 typedef struct {
     int kind;
     int decimal_places;
@@ -235,6 +239,14 @@ typedef struct {
 } falcon_synth_spec;
 falcon_status falcon_synth_fill(int precision, const falcon_synth_spec* spec, void* out,
                                 uint64_t count);
+/* Values [first, first + count) of the stream.  first > 0 needs a counter-based kind
+ * (FALCON_KIND_FIELD); the reference's kinds are sequential (synthetic.hpp:111). */
+falcon_status falcon_synth_fill_at(int precision, const falcon_synth_spec* spec, uint64_t first,
+                                   void* out, uint64_t count);
+/* Device twin of falcon_synth_fill_at for counter-based kinds: writes d_out (device) on
+ * `stream` (asynchronous).  Other kinds: FALCON_ERR_UNSUPPORTED. */
+falcon_status falcon_synth_device(falcon_ctx* ctx, int precision, const falcon_synth_spec* spec,
+                                  uint64_t first, void* d_out, uint64_t count, void* stream);
 
 #ifdef __cplusplus
 }

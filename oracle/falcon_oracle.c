@@ -494,7 +494,34 @@ static uint64_t mt64_next(mt64* m) {
     return y;
 }
 
+/* Counter-based "HPC field" of the sharded configs.  Not a reference kind: pinned by the
+ * product's csrc/field.cuh (restated here independently, bit for bit): two integer
+ * triangle waves plus splitmix64 noise, quantised to decimal_places. */
+static uint64_t or_field_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+static int64_t or_tri(uint64_t x, uint64_t period, int64_t amp) {
+    const uint64_t half = period / 2, r = x % period;
+    return amp * (int64_t)(r < half ? r : period - r) / (int64_t)half;
+}
+int or_synth_fill_at(int prec, const or_spec* s, uint64_t first, void* out, uint64_t count) {
+    if (s->kind != OR_KIND_FIELD) return first == 0 ? or_synth_fill(prec, s, out, count) : -1;
+    if (s->decimal_places < 0 || s->decimal_places > (prec == 0 ? 22 : 10)) return -1;
+    for (uint64_t i = 0; i < count; ++i) {
+        const uint64_t x = first + i;
+        const uint64_t h = or_field_mix(x + (s->seed + 1) * 0x9E3779B97F4A7C15ULL);
+        const int64_t units = or_tri(x, 65536, 50000) + or_tri(x, 1048573, 400000) - 225000 +
+                              ((int64_t)(h % 127) - 63);
+        if (prec == 0) ((double*)out)[i] = or_inverse_scale_f64(units, s->decimal_places);
+        else ((float*)out)[i] = or_inverse_scale_f32(units, s->decimal_places);
+    }
+    return 0;
+}
+
 int or_synth_fill(int prec, const or_spec* s, void* out, uint64_t count) {
+    if (s->kind == OR_KIND_FIELD) return or_synth_fill_at(prec, s, 0, out, count);
     const int max_alpha = prec == 0 ? 22 : 10, max_beta = prec == 0 ? 15 : 6;
     if (s->decimal_places < 0 || s->decimal_places > max_alpha) return -1;
     if (s->max_step_units < 1) return -1;

@@ -112,7 +112,7 @@ int or_decompress_archive(int prec, const uint8_t* in, uint64_t len, void* value
 
 /* ---- synthetic.hpp generators (synthetic.hpp:36-115) + the pinned cfg3 kind ---- */
 enum { OR_KIND_WALK = 0, OR_KIND_DECIMAL = 1, OR_KIND_SIGNFLIP = 2, OR_KIND_OUTLIER = 3,
-       OR_KIND_BITS = 4, OR_KIND_MIXED_BLOCKS = 5 };
+       OR_KIND_BITS = 4, OR_KIND_MIXED_BLOCKS = 5, OR_KIND_FIELD = 6 };
 typedef struct {
     int kind;
     int decimal_places;
@@ -123,6 +123,8 @@ typedef struct {
     uint32_t block;         /* MIXED_BLOCKS only: values per decimal-place block */
 } or_spec;
 int or_synth_fill(int prec, const or_spec* s, void* out, uint64_t count);
+/* Counter-based kinds (OR_KIND_FIELD) from any absolute value index `first`. */
+int or_synth_fill_at(int prec, const or_spec* s, uint64_t first, void* out, uint64_t count);
 
 #ifdef __cplusplus
 }

@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libfalcon_ref.so")
 
-KINDS = {"walk": 0, "decimal": 1, "signflip": 2, "outlier": 3, "bits": 4, "mixed": 5}
+KINDS = {"walk": 0, "decimal": 1, "signflip": 2, "outlier": 3, "bits": 4, "mixed": 5, "field": 6}
 F64, F32 = 0, 1
 
 
@@ -76,6 +76,7 @@ class Oracle:
                                             C.c_uint64, C.POINTER(C.c_uint64),
                                             C.POINTER(C.c_uint64)]
         L.or_synth_fill.argtypes = [C.c_int, C.POINTER(_Spec), C.c_void_p, C.c_uint64]
+        L.or_synth_fill_at.argtypes = [C.c_int, C.POINTER(_Spec), C.c_uint64, C.c_void_p, C.c_uint64]
         L.or_dp_alpha_batch.argtypes = [C.c_int, C.c_void_p, C.c_uint64, C.c_void_p]
         L.or_round_scale_f64.argtypes = [C.c_double, C.c_int, C.POINTER(C.c_int64)]
         L.or_round_scale_f32.argtypes = [C.c_float, C.c_int, C.POINTER(C.c_int64)]
@@ -162,10 +163,12 @@ class Oracle:
         return out[: n.value]
 
     def synth(self, kind: str, count: int, prec: int = F64, dp: int = 2, seed: int = 1,
-              step: int = 127, period: int = 1025, units: int = 3575, block: int = 1025) -> np.ndarray:
+              step: int = 127, period: int = 1025, units: int = 3575, block: int = 1025,
+              first: int = 0, out: np.ndarray | None = None) -> np.ndarray:
         s = _Spec(KINDS[kind], dp, seed, step, period, units, block)
-        out = np.zeros(count, dtype_of(prec))
-        if self.lib.or_synth_fill(prec, C.byref(s), _ptr(out), count):
+        if out is None:
+            out = np.zeros(count, dtype_of(prec))
+        if self.lib.or_synth_fill_at(prec, C.byref(s), first, _ptr(out), count):
             raise ValueError("bad generator spec")
         return out
 

@@ -21,7 +21,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
          "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I", os.path.join(ROOT, "include")]
 UNITS = ["kernels_all.cu", "capi.cu", "runtime.cu", "pipeline.cu"]
-HEADERS = ["falcon_common.cuh", "kernels.h", "runtime.h", "encode.cu", "decode.cu", "tables.cu"]
+HEADERS = ["falcon_common.cuh", "kernels.h", "runtime.h", "encode.cu", "decode.cu", "tables.cu", "selftest.cu",
+           "synth.cu", "field.cuh", "dpds.cuh", "launch_cache.cuh"]
 
 
 def _mtime(p: str) -> float:

@@ -4,6 +4,7 @@
 #include <mutex>
 #include <random>
 
+#include "field.cuh"
 #include "runtime.h"
 
 namespace fb200 {
@@ -490,7 +491,44 @@ falcon_status falcon_decompress_chunk(falcon_ctx* ctx, int precision, const uint
 }
 
 // ---- synthetic generators (synthetic.hpp:36-115) ------------------------------------
+falcon_status falcon_synth_fill_at(int precision, const falcon_synth_spec* s, uint64_t first, void* out,
+                                   uint64_t count) {
+    if (s->kind != FALCON_KIND_FIELD) {
+        if (first != 0)
+            return set_error(FALCON_ERR_INVALID, "only counter-based generator kinds start at an offset");
+        return falcon_synth_fill(precision, s, out, count);
+    }
+    if (s->decimal_places < 0 || s->decimal_places > (precision == FALCON_F64 ? 22 : 10))
+        return set_error(FALCON_ERR_INVALID, "decimal_places out of range for this precision");
+    double p64 = 1;
+    float p32 = 1;
+    for (int i = 0; i < s->decimal_places; ++i) {
+        p64 *= 10;
+        p32 *= 10;
+    }
+    for (uint64_t i = 0; i < count; ++i) {
+        const int64_t u = field_units(s->seed, first + i);
+        if (precision == FALCON_F64) static_cast<double*>(out)[i] = (double)u / p64;
+        else static_cast<float*>(out)[i] = (float)u / p32;
+    }
+    return FALCON_OK;
+}
+
+falcon_status falcon_synth_device(falcon_ctx* ctx, int precision, const falcon_synth_spec* s, uint64_t first,
+                                  void* d_out, uint64_t count, void* stream) {
+    if (!ctx || !s) return set_error(FALCON_ERR_INVALID, "null argument");
+    if (s->kind != FALCON_KIND_FIELD)
+        return set_error(FALCON_ERR_UNSUPPORTED, "the device generator supports counter-based kinds only");
+    if (s->decimal_places < 0 || s->decimal_places > (precision == FALCON_F64 ? 22 : 10))
+        return set_error(FALCON_ERR_INVALID, "decimal_places out of range for this precision");
+    device_guard dg(ctx->device);
+    FB_CUDA(launch_field(precision, d_out, first, count, s->seed, s->decimal_places,
+                         static_cast<cudaStream_t>(stream)));
+    return FALCON_OK;
+}
+
 falcon_status falcon_synth_fill(int precision, const falcon_synth_spec* s, void* out, uint64_t count) {
+    if (s->kind == FALCON_KIND_FIELD) return falcon_synth_fill_at(precision, s, 0, out, count);
     const int max_alpha = precision == FALCON_F64 ? 22 : 10;
     const int max_beta = precision == FALCON_F64 ? 15 : 6;
     if (s->decimal_places < 0 || s->decimal_places > max_alpha)

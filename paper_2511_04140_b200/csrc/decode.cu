@@ -940,13 +940,13 @@ cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry
     default: kern = nullptr;
     }
     if (!kern) return cudaErrorInvalidConfiguration;
-    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    if ((e = ensure_dynamic_smem((const void*)kern, smem))) return e;
     // persistent grid, every block co-resident; the walker kernel goes first and lets the
-    // decoder launch immediately (programmatic dependent launch)
-    int per_sm = 0, dev = 0, sms = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (int)threads + 32 * decode_cfg<T>::producers, smem))) return e;
-    if ((e = cudaGetDevice(&dev))) return e;
-    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev))) return e;
+    // decoder launch immediately (programmatic dependent launch).  Occupancy and SM count
+    // are cached per (device, kernel, smem): no queries per call.
+    int per_sm = 0, sms = 0;
+    if ((e = resident_blocks((const void*)kern, (int)threads + 32 * decode_cfg<T>::producers, smem, &per_sm, &sms)))
+        return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     uint64_t grid = (uint64_t)per_sm * sms;
     if (grid > g.n_chunks) grid = g.n_chunks;
@@ -955,7 +955,7 @@ cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry
     uint32_t cap = g.cpb + 64 < (24u << 10) ? g.cpb + 64 : (24u << 10);
     cap = (cap + 3) & ~3u;
     const size_t wsm = 8 * (size_t)cap + 48;
-    if ((e = cudaFuncSetAttribute(walker_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm))) return e;
+    if ((e = ensure_dynamic_smem((const void*)walker_kernel, (uint32_t)wsm))) return e;
     if (ev0 && (e = cudaEventRecord(ev0, st))) return e;
     const uint32_t emax = (uint32_t)(lane_traits<T>::header + (lane_traits<T>::width + 7) / 8 +
                                       lane_traits<T>::width * ((g.chunk_n - 1) / 8));  // max_encoded_chunk_size

@@ -27,6 +27,8 @@
 #include "falcon_common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace fb200 {
 
 namespace {
@@ -85,10 +87,14 @@ template <typename T, int NT>
 constexpr int encode_min_blocks() {
     return NT <= 128 ? (sizeof(T) == 4 ? FB_ENC_MIN_BLOCKS32 : FB_ENC_MIN_BLOCKS) : (2048 / NT > 0 ? 2048 / NT : 1);
 }
+template <int NT, int U>
+__device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_t out_cap, const encode_ws& ws,
+                           const encode_launch& L, const archive_header_bytes& hdr, uint8_t* smem);
+
 template <typename T, int NT>
 __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     encode_chunks_kernel(const T* __restrict__ in, geometry g, uint8_t* __restrict__ out,
-                         uint64_t out_cap, encode_ws ws) {
+                         uint64_t out_cap, encode_ws ws, encode_launch L, archive_header_bytes hdr) {
     using tr = lane_traits<T>;
     using X = fpx<T>;
     using B = typename tr::B;
@@ -117,8 +123,16 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     __shared__ uint32_t s_size;
     __shared__ B s_z1;
 
-    // grid: x = chunk in batch, y + 65535 z = batch (no integer division)
-    const uint32_t b = blockIdx.y + 65535u * blockIdx.z;
+    // grid row 0: placement of the tiles the previous launches finished encoding (their
+    // images sit in the ring; see launch_encode); rows 1..: x = chunk in batch, y - 1 =
+    // batch of this wave (no integer division)
+    if (blockIdx.y == 0) {
+        // beside encode CTAs: 2 vectors per lane in flight (f64, 56 registers), 1 for f32
+        // (32 registers)
+        if (blockIdx.x < L.place_tiles) place_tile<NT, sizeof(T) == 8 ? 2 : 1>(g, out, out_cap, ws, L, hdr, smem);
+        return;
+    }
+    const uint32_t b = L.b0 + blockIdx.y - 1;
     const uint32_t ci = blockIdx.x;
     if (b >= g.n_batches || ci >= g.chunks_in(b)) return;  // uniform per CTA
     const uint32_t c = b * g.cpb + ci;                      // < 2^31 chunks per launch
@@ -490,29 +504,35 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     }
     __syncthreads();
 
-    // ---- store the image into this chunk's scratch slot (16-B aligned) ----
-    uint4* dst = reinterpret_cast<uint4*>(ws.images + c * (uint64_t)ws.slot);
+    // ---- store the image into this chunk's ring slot (16-B aligned) ----
+    uint32_t slot = L.enc_slot0 + (c - L.enc_c0);   // = c mod ring (no division)
+    slot = slot >= ws.ring ? slot - (uint32_t)ws.ring : slot;
+    uint4* dst = reinterpret_cast<uint4*>(ws.images + slot * (uint64_t)ws.slot);
     const uint4* srcv = reinterpret_cast<const uint4*>(s_stage);
     const uint32_t nvec = (size + 15) >> 4;
     for (uint32_t vv = tid; vv < nvec; vv += NT) dst[vv] = srcv[vv];
 }
 
-// Placement: chunk images -> archive.  A tile of kPlaceTile consecutive chunks per CTA;
+// Placement: chunk images -> archive.  A tile of NT consecutive chunks per CTA (grid row 0
+// of an encode launch, beside the next wave's encode CTAs);
 // sizes are known up front, so every tile publishes its aggregate at once and the
 // decoupled look-back never waits on compute.  The tile then writes its chunks'
 // size-table entries (container.cpp:88-111), copies each image to
 // chunk_base(c) + exclusive prefix with funnel-shifted 16-B stores, and the first
 // tile writes the 47-byte header (container.cpp:44-55).
-__global__ void __launch_bounds__(kPlaceTile) place_chunks_kernel(geometry g, uint8_t* __restrict__ out,
-                                                                  uint64_t out_cap, encode_ws ws,
-                                                                  archive_header_bytes hdr) {
+template <int NT, int U>
+__device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_t out_cap, const encode_ws& ws,
+                           const encode_launch& L, const archive_header_bytes& hdr, uint8_t* smem) {
+    constexpr int kPlaceTile = NT;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = kPlaceTile / 32;
+    // carved from the encode kernel's dynamic smem (placement_smem_bytes)
+    uint64_t* s_off = reinterpret_cast<uint64_t*>(smem);                       // [NT]
+    uint32_t* s_sz = reinterpret_cast<uint32_t*>(s_off + kPlaceTile);          // [NT]
+    uint32_t (*s_vpre)[33] = reinterpret_cast<uint32_t (*)[33]>(s_sz + kPlaceTile);  // [NW][33]
     __shared__ uint32_t s_ticket;
     __shared__ uint32_t s_wsum[NW];
     __shared__ uint64_t s_tile_excl;
-    __shared__ uint64_t s_off[kPlaceTile];
-    __shared__ uint32_t s_sz[kPlaceTile];
     if (tid == 0) s_ticket = atomicAdd(ws.ticket, 1u);
     __syncthreads();
     const uint64_t t = s_ticket;
@@ -612,7 +632,6 @@ __global__ void __launch_bounds__(kPlaceTile) place_chunks_kernel(geometry g, ui
     // copy: each warp moves its 32 chunks as one flat list of destination vectors, so a
     // lane's consecutive vectors are independent (their loads overlap) instead of the
     // chunks being copied one after another
-    __shared__ uint32_t s_vpre[kPlaceTile / 32][33];
     {
         const int idx = warp * 32 + lane;
         const uint64_t cc = t * kPlaceTile + idx;
@@ -635,34 +654,66 @@ __global__ void __launch_bounds__(kPlaceTile) place_chunks_kernel(geometry g, ui
     }
     const uint32_t V = s_vpre[warp][32];
     int k = 0;  // this lane's current chunk (vectors are visited in increasing order)
-    for (uint32_t gv = lane; gv < V; gv += 32) {
-        while (gv >= s_vpre[warp][k + 1]) ++k;
-        const int idx = warp * 32 + k;
-        const uint64_t cc = t * kPlaceTile + idx;
-        const uint64_t off = s_off[idx];
-        const uint32_t size = s_sz[idx];
-        const uint32_t* img = reinterpret_cast<const uint32_t*>(ws.images + cc * (uint64_t)ws.slot);
-        const uint32_t a = (uint32_t)(off & 15);
-        uint8_t* dstb = out + (off - a);
-        const uint32_t end = a + size;
-        const uint32_t vv = gv - s_vpre[warp][k];
-        const uint32_t lo = vv << 4, hi = lo + 16;
-        if (lo >= a && hi <= end) {
-            // destination bytes [lo, lo+16) = image bytes [lo - a, lo - a + 16)
-            const uint32_t sb = lo - a;
-            const uint32_t w0 = sb >> 2, sh = (sb & 3) * 8;
-            uint32_t r[5];
+    // U vectors per lane in flight: all their loads are issued before the first store
+    // (a lane's copy is otherwise a chain of ~V/32 dependent DRAM round trips)
+    for (uint32_t gv0 = lane; gv0 < V; gv0 += 32 * U) {
+        uint32_t r[U][5];
+        uint8_t* dst[U];
+        const uint8_t* src[U];
+        uint32_t sh[U], from[U], to[U];
+        bool vec[U];
 #pragma unroll
-            for (int i = 0; i < 5; ++i) r[i] = __ldg(img + w0 + i);
-            *reinterpret_cast<uint4*>(dstb + lo) =
-                make_uint4(__funnelshift_r(r[0], r[1], sh), __funnelshift_r(r[1], r[2], sh),
-                           __funnelshift_r(r[2], r[3], sh), __funnelshift_r(r[3], r[4], sh));
-        } else {
-            const uint8_t* ib = reinterpret_cast<const uint8_t*>(img);
-            const uint32_t from = lo > a ? lo : a, to = hi < end ? hi : end;
-            for (uint32_t i = from; i < to; ++i) dstb[i] = ib[i - a];
+        for (int u = 0; u < U; ++u) {
+            const uint32_t gv = gv0 + 32 * u;
+            vec[u] = false;
+            from[u] = to[u] = 0;
+            if (gv >= V) continue;
+            while (gv >= s_vpre[warp][k + 1]) ++k;
+            const int idx = warp * 32 + k;
+            const uint64_t cc = t * kPlaceTile + idx;
+            const uint64_t off = s_off[idx];
+            uint32_t rs = L.place_slot0 + (uint32_t)(cc - L.place_c0);   // = cc mod ring
+            rs = rs >= ws.ring ? rs - (uint32_t)ws.ring : rs;
+            const uint8_t* img = ws.images + rs * (uint64_t)ws.slot;
+            const uint32_t a = (uint32_t)(off & 15);
+            const uint32_t end = a + s_sz[idx];
+            const uint32_t lo = (gv - s_vpre[warp][k]) << 4, hi = lo + 16;
+            dst[u] = out + (off - a) + lo;
+            if (lo >= a && hi <= end) {
+                // destination bytes [lo, lo+16) = image bytes [lo - a, lo - a + 16)
+                const uint32_t sb = lo - a;
+                const uint32_t* w = reinterpret_cast<const uint32_t*>(img) + (sb >> 2);
+                sh[u] = (sb & 3) * 8;
+#pragma unroll
+                for (int i = 0; i < 5; ++i) r[u][i] = __ldg(w + i);
+                vec[u] = true;
+            } else {
+                from[u] = lo > a ? lo : a;
+                to[u] = hi < end ? hi : end;
+                src[u] = img + from[u] - a;
+                dst[u] += (int)(from[u] - lo);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (vec[u]) {
+                *reinterpret_cast<uint4*>(dst[u]) =
+                    make_uint4(__funnelshift_r(r[u][0], r[u][1], sh[u]), __funnelshift_r(r[u][1], r[u][2], sh[u]),
+                               __funnelshift_r(r[u][2], r[u][3], sh[u]), __funnelshift_r(r[u][3], r[u][4], sh[u]));
+            } else {
+                for (uint32_t i = 0; i < to[u] - from[u]; ++i) dst[u][i] = src[u][i];
+            }
         }
     }
+}
+
+// The final placement of a compress call (tiles of the last wave), no encode beside it:
+// a lane keeps 4 vectors in flight.
+template <int NT>
+__global__ void __launch_bounds__(NT) place_final_kernel(geometry g, uint8_t* __restrict__ out, uint64_t out_cap,
+                                                         encode_ws ws, encode_launch L, archive_header_bytes hdr) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    place_tile<NT, 4>(g, out, out_cap, ws, L, hdr, smem);
 }
 
 // one thread per byte column, rounded to an instantiated CTA size
@@ -675,9 +726,10 @@ uint32_t encode_block_threads(uint32_t chunk_n) {
 template <typename T>
 uint32_t encode_smem_bytes(uint32_t chunk_n) {
     using tr = lane_traits<T>;
-    const uint32_t nc = (chunk_n - 1) / 8;
-    (void)nc;
-    return encode_stage_bytes<T>(chunk_n) + (tr::width / 8) * encode_block_threads(chunk_n) * 8;
+    const uint32_t nt = encode_block_threads(chunk_n);
+    const uint32_t enc = encode_stage_bytes<T>(chunk_n) + (tr::width / 8) * nt * 8;
+    const uint32_t place = 12 * nt + 4 * 33 * (nt / 32);   // place_tile's carve-out
+    return enc > place ? enc : place;
 }
 
 template <typename T>
@@ -689,15 +741,48 @@ uint32_t encode_slot_bytes(uint32_t chunk_n) {
     return (uint32_t)(tr::header + (tr::width + 7) / 8 + tr::width * nc + 4 + 15) & ~15u;
 }
 
+// Waves: one encode launch covers `wave` batches; its grid row 0 places the tiles the
+// previous launches finished (a final place-only launch takes the rest).  Images live in a
+// ring of `ring` slots, so scratch is O(wave), not O(input): launch k writes chunks
+// [c_k, c_k + wave chunks) while placing chunks in [c_{k-1} - tile, c_k); a ring of
+// 2 * wave chunks + one tile keeps the two sets apart.
+struct wave_plan {
+    uint64_t wave_batches, launches, ring, tiles, tile;
+};
+
+static uint64_t env_wave_chunks() {
+    static const uint64_t v = [] {
+        const char* e = std::getenv("FALCON_ENC_WAVE_CHUNKS");
+        const unsigned long long x = e ? std::strtoull(e, nullptr, 10) : 0ull;
+        return (uint64_t)(x ? x : 49152ull);   // 12 default batches
+    }();
+    return v;
+}
+
+static wave_plan plan_waves(const geometry& g) {
+    wave_plan w;
+    w.tile = encode_block_threads(g.chunk_n);
+    w.tiles = (g.n_chunks + w.tile - 1) / w.tile;
+    uint64_t wb = env_wave_chunks() / g.cpb;
+    if (wb < 1) wb = 1;
+    if (wb > 65534) wb = 65534;                     // grid.y = 1 + batches of the wave
+    if (wb >= g.n_batches) wb = g.n_batches;
+    w.wave_batches = wb ? wb : 1;
+    w.launches = g.n_batches ? (g.n_batches + w.wave_batches - 1) / w.wave_batches : 0;
+    const uint64_t need = 2 * w.wave_batches * g.cpb + w.tile;
+    w.ring = w.launches <= 1 || need >= g.n_chunks ? (g.n_chunks ? g.n_chunks : 1) : need;
+    return w;
+}
+
 template <typename T>
 size_t encode_scratch_bytes(const geometry& g) {
-    const uint64_t tiles = (g.n_chunks + kPlaceTile - 1) / kPlaceTile;
+    const wave_plan w = plan_waves(g);
     size_t b = 0;
     b += (g.n_chunks * 4 + 15) & ~15ull;                 // sizes
-    b += tiles * 8;                                       // tile status
+    b += w.tiles * 8;                                     // tile status
     b += (g.n_batches + 1) * 8;                           // batch prefixes
     b = (b + 255) & ~255ull;
-    b += g.n_chunks * (uint64_t)encode_slot_bytes<T>(g.chunk_n);  // images
+    b += w.ring * (uint64_t)encode_slot_bytes<T>(g.chunk_n);  // image ring
     return b;
 }
 
@@ -705,22 +790,38 @@ template <typename T>
 encode_ws carve_encode_ws(void* scratch, const geometry& g, uint32_t* ticket, unsigned long long* error,
                           uint64_t* total) {
     encode_ws ws;
+    const wave_plan w = plan_waves(g);
     uint8_t* p = static_cast<uint8_t*>(scratch);
-    const uint64_t tiles = (g.n_chunks + kPlaceTile - 1) / kPlaceTile;
     ws.sizes = reinterpret_cast<uint32_t*>(p);
     p += (g.n_chunks * 4 + 15) & ~15ull;
     ws.tile_status = reinterpret_cast<uint64_t*>(p);
-    p += tiles * 8;
+    p += w.tiles * 8;
     ws.batch_prefix = reinterpret_cast<uint64_t*>(p);
     p += (g.n_batches + 1) * 8;
     const size_t used = (size_t)(p - static_cast<uint8_t*>(scratch));
     p = static_cast<uint8_t*>(scratch) + ((used + 255) & ~255ull);
     ws.images = p;
     ws.slot = encode_slot_bytes<T>(g.chunk_n);
+    ws.ring = w.ring;
     ws.ticket = ticket;
     ws.error = error;
     ws.total = total;
     return ws;
+}
+
+static cudaError_t launch_place_final(uint32_t threads, uint32_t tiles, const geometry& g, uint8_t* d_out,
+                                      uint64_t out_cap, const encode_ws& ws, const encode_launch& L,
+                                      const archive_header_bytes& hdr, cudaStream_t st) {
+    const uint32_t smem = 12 * threads + 4 * 33 * (threads / 32);
+    switch (threads) {
+#define FB_PLACE(n) \
+    case n: place_final_kernel<n><<<tiles, n, smem, st>>>(g, d_out, out_cap, ws, L, hdr); break;
+    FB_PLACE(32) FB_PLACE(64) FB_PLACE(96) FB_PLACE(128) FB_PLACE(160) FB_PLACE(192) FB_PLACE(224)
+    FB_PLACE(256) FB_PLACE(512)
+#undef FB_PLACE
+    default: return cudaErrorInvalidConfiguration;
+    }
+    return cudaGetLastError();
 }
 
 template <typename T>
@@ -734,13 +835,13 @@ cudaError_t launch_encode(const T* d_in, const geometry& g, uint8_t* d_out, uint
             return e;
         return g.header_bytes ? cudaMemcpyAsync(d_out, hdr.b, 47, cudaMemcpyHostToDevice, st) : cudaSuccess;
     }
-    const uint64_t tiles = (g.n_chunks + kPlaceTile - 1) / kPlaceTile;
+    const wave_plan w = plan_waves(g);
     // tile status + batch prefixes are contiguous
-    if ((e = cudaMemsetAsync(ws.tile_status, 0, (tiles + g.n_batches + 1) * 8, st))) return e;
+    if ((e = cudaMemsetAsync(ws.tile_status, 0, (w.tiles + g.n_batches + 1) * 8, st))) return e;
     if ((e = cudaMemsetAsync(ws.ticket, 0, sizeof(uint32_t), st))) return e;
     const uint32_t threads = encode_block_threads(g.chunk_n);
     const uint32_t smem = encode_smem_bytes<T>(g.chunk_n);
-    void (*kern)(const T*, geometry, uint8_t*, uint64_t, encode_ws);
+    void (*kern)(const T*, geometry, uint8_t*, uint64_t, encode_ws, encode_launch, archive_header_bytes);
     switch (threads) {
     case 32: kern = encode_chunks_kernel<T, 32>; break;
     case 64: kern = encode_chunks_kernel<T, 64>; break;
@@ -755,14 +856,35 @@ cudaError_t launch_encode(const T* d_in, const geometry& g, uint8_t* d_out, uint
     default: kern = nullptr;
     }
     if (!kern) return cudaErrorInvalidConfiguration;
-    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    if ((e = ensure_dynamic_smem((const void*)kern, smem))) return e;
     if (ev0 && (e = cudaEventRecord(ev0, st))) return e;
-    const dim3 grid(g.cpb, (unsigned)(g.n_batches < 65535 ? g.n_batches : 65535), (unsigned)((g.n_batches + 65534) / 65535));
-    kern<<<grid, threads, smem, st>>>(d_in, g, d_out, out_cap, ws);
-    if ((e = cudaGetLastError())) return e;
-    if (ev1 && (e = cudaEventRecord(ev1, st))) return e;
-    place_chunks_kernel<<<(unsigned)tiles, kPlaceTile, 0, st>>>(g, d_out, out_cap, ws, hdr);
-    return cudaGetLastError();
+    uint64_t placed = 0;
+    for (uint64_t k = 0; k <= w.launches; ++k) {
+        encode_launch L;
+        const uint64_t b0 = k * w.wave_batches;
+        L.b0 = (uint32_t)(k < w.launches ? b0 : 0);
+        const uint64_t nb = k < w.launches ? (g.n_batches - b0 < w.wave_batches ? g.n_batches - b0 : w.wave_batches) : 0;
+        // tiles whose chunks all were encoded by launches < k
+        const uint64_t done_chunks = k < w.launches ? b0 * g.cpb : g.n_chunks;
+        const uint64_t placeable = k < w.launches ? done_chunks / w.tile : w.tiles;
+        L.place_tiles = (uint32_t)(placeable - placed);
+        // ring slots without a division in the kernel: slot(c) = slot0 + (c - c0), wrapped once
+        L.enc_c0 = (uint32_t)(b0 * g.cpb);
+        L.enc_slot0 = (uint32_t)((b0 * g.cpb) % w.ring);
+        L.place_c0 = (uint32_t)(placed * w.tile);
+        L.place_slot0 = (uint32_t)((placed * w.tile) % w.ring);
+        if (nb == 0 && L.place_tiles == 0) continue;
+        if (nb == 0) {
+            e = launch_place_final(threads, L.place_tiles, g, d_out, out_cap, ws, L, hdr, st);
+        } else {
+            const unsigned gx = (unsigned)(g.cpb > L.place_tiles ? g.cpb : L.place_tiles);
+            kern<<<dim3(gx, (unsigned)(1 + nb)), threads, smem, st>>>(d_in, g, d_out, out_cap, ws, L, hdr);
+            e = cudaGetLastError();
+        }
+        if (e) return e;
+        placed = placeable;
+    }
+    return ev1 ? cudaEventRecord(ev1, st) : cudaSuccess;
 }
 
 template cudaError_t launch_encode<double>(const double*, const geometry&, uint8_t*, uint64_t,

@@ -15,7 +15,8 @@ struct archive_header_bytes {
 // Scratch for one compress launch (device memory, owned by the caller/context).
 // Carved out of one buffer by carve_encode_ws(); encode_scratch_bytes() sizes it.
 struct encode_ws {
-    uint8_t* images;              // [n_chunks][slot] chunk images (16-B aligned slots)
+    uint8_t* images;              // [ring][slot] chunk images (16-B aligned slots), chunk c at c % ring
+    uint64_t ring;                // image slots (O(wave), launch_encode)
     uint32_t slot;                // bytes per image slot
     uint32_t* sizes;              // [n_chunks] encoded chunk sizes
     uint64_t* tile_status;        // [n_tiles] placement look-back words
@@ -25,7 +26,14 @@ struct encode_ws {
     uint64_t* total;              // archive bytes, written by the placement kernel
 };
 
-constexpr uint32_t kPlaceTile = 256;  // chunks per placement tile
+// One encode launch: batches [b0, b0 + gridDim.y - 1) are encoded, and grid row 0 places
+// `place_tiles` tiles (of blockDim.x chunks) that earlier launches finished.
+struct encode_launch {
+    uint32_t b0;
+    uint32_t place_tiles;
+    uint32_t enc_c0, enc_slot0;       // first chunk encoded here and its ring slot
+    uint32_t place_c0, place_slot0;   // first chunk placed here and its ring slot
+};
 template <typename T> uint32_t encode_slot_bytes(uint32_t chunk_n);
 template <typename T> size_t encode_scratch_bytes(const geometry& g);
 template <typename T>
@@ -67,6 +75,10 @@ cudaError_t launch_selftest_dp(int prec, const void* v, uint64_t n, int A, int8_
                                int8_t* lit, int8_t* cert, int64_t* g, cudaStream_t st);
 
 cudaError_t launch_selftest_div(int prec, const int64_t* g, uint64_t n, int alpha, void* out, cudaStream_t st);
+
+// Counter-based field generator (field.cuh): values [first, first + count) into out.
+cudaError_t launch_field(int prec, void* out, uint64_t first, uint64_t count, uint64_t seed, int dp,
+                         cudaStream_t st);
 
 // One-time upload of the pow10 / decade tables (numeric.hpp:17-41, numeric.cpp:10-39).
 cudaError_t upload_tables();

@@ -1,6 +1,7 @@
 // runtime.cu -- status plumbing, format helpers, buffers, worker pool, slots.
+#include <algorithm>
+#include <cerrno>
 #include <cstdlib>
-#include <charconv>
 
 #include "runtime.h"
 
@@ -154,47 +155,86 @@ bool is_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
-// ---- worker pool ---------------------------------------------------------------
-worker_pool::worker_pool(unsigned workers) {
-    if (workers == 0) workers = default_workers();
-    for (unsigned i = 0; i < workers; ++i) threads_.emplace_back([this] { run(); });
+// ---- task pool ---------------------------------------------------------------------
+worker_pool::worker_pool(unsigned workers) : ring_(1024) {
+    const unsigned n = workers ? workers : default_workers();
+    threads_.reserve(n);
+    while (threads_.size() < n) threads_.emplace_back(&worker_pool::worker_main, this);
 }
+
 worker_pool::~worker_pool() {
     {
-        std::lock_guard<std::mutex> l(m_);
-        stop_ = true;
+        std::unique_lock<std::mutex> g(lock_);
+        closing_ = true;
     }
-    cv_.notify_all();
-    for (auto& t : threads_) t.join();
+    has_job_.notify_all();
+    has_room_.notify_all();
+    for (std::thread& t : threads_) t.join();
 }
+
 void worker_pool::submit(std::function<void()> job) {
-    {
-        std::lock_guard<std::mutex> l(m_);
-        q_.push_back(std::move(job));
-    }
-    cv_.notify_one();
+    std::unique_lock<std::mutex> g(lock_);
+    has_room_.wait(g, [&] { return tail_ - head_ < ring_.size(); });
+    ring_[tail_++ % ring_.size()] = std::move(job);
+    g.unlock();
+    has_job_.notify_one();
 }
-void worker_pool::run() {
+
+void worker_pool::worker_main() {
+    std::unique_lock<std::mutex> g(lock_);
     for (;;) {
-        std::function<void()> job;
-        {
-            std::unique_lock<std::mutex> l(m_);
-            cv_.wait(l, [&] { return stop_ || !q_.empty(); });
-            if (q_.empty()) return;
-            job = std::move(q_.front());
-            q_.pop_front();
-        }
+        has_job_.wait(g, [&] { return closing_ || head_ != tail_; });
+        if (head_ == tail_) return;          // closing and drained
+        std::function<void()> job = std::move(ring_[head_++ % ring_.size()]);
+        g.unlock();
+        has_room_.notify_one();
         job();
+        g.lock();
     }
 }
+
+void worker_pool::fork_join(unsigned parts, const std::function<void(unsigned)>& fn) {
+    if (parts <= 1 || threads_.empty()) {
+        for (unsigned i = 0; i < parts; ++i) fn(i);
+        return;
+    }
+    // parts are claimed from a shared counter by the helpers and the caller alike, so a
+    // busy pool never stalls the caller
+    struct join_state {
+        std::atomic<unsigned> next{0}, left;
+        std::mutex m;
+        std::condition_variable cv;
+        explicit join_state(unsigned n) : left(n) {}
+    };
+    auto st = std::make_shared<join_state>(parts);
+    auto drain = [st, parts, &fn] {
+        for (unsigned i; (i = st->next.fetch_add(1)) < parts;) {
+            fn(i);
+            if (st->left.fetch_sub(1) == 1) {
+                std::lock_guard<std::mutex> g(st->m);
+                st->cv.notify_all();
+            }
+        }
+    };
+    const unsigned helpers = std::min<unsigned>(parts - 1, (unsigned)threads_.size());
+    for (unsigned h = 0; h < helpers; ++h) submit(drain);
+    drain();
+    std::unique_lock<std::mutex> g(st->m);
+    st->cv.wait(g, [&] { return st->left.load() == 0; });
+}
+
 unsigned worker_pool::default_workers() {
+    // FALCON_WORKERS: a positive decimal integer, anything else is ignored
+    // (worker_pool.hpp:30-38 default)
     if (const char* env = std::getenv("FALCON_WORKERS")) {
-        unsigned v = 0;
-        const auto r = std::from_chars(env, env + std::strlen(env), v);
-        if (r.ec == std::errc{} && *r.ptr == '\0' && v > 0) return v;
+        char* end = nullptr;
+        errno = 0;
+        const unsigned long v = std::strtoul(env, &end, 10);
+        if (errno == 0 && end != env && *end == '\0' && v > 0 && v <= 4096 && env[0] != '-')
+            return (unsigned)v;
     }
     const unsigned hw = std::thread::hardware_concurrency();
-    return hw ? hw : 1;
+    return hw > 0 ? hw : 1;
 }
 
 // ---- slots ---------------------------------------------------------------------

@@ -72,22 +72,30 @@ struct pinned_buffer {
 
 bool is_pinned(const void* p);
 
-// ---- host worker pool (same contract as the reference's worker_pool:
-//      include/falcon/worker_pool.hpp:14-38, FALCON_WORKERS env) -------------------
+// ---- host task pool ------------------------------------------------------------
+// Contract of the reference's worker_pool (include/falcon/worker_pool.hpp:14-38): N
+// threads (0 = FALCON_WORKERS or the hardware thread count), FIFO jobs, joined on
+// destruction.  Built here as a fixed-capacity ring of jobs plus a fork-join helper the
+// pipeline uses to split pageable staging copies across threads.
 class worker_pool {
 public:
     explicit worker_pool(unsigned workers);
     ~worker_pool();
+    worker_pool(const worker_pool&) = delete;
+    worker_pool& operator=(const worker_pool&) = delete;
     void submit(std::function<void()> job);
+    // run fn(0..parts-1) on the pool and the calling thread; returns when all are done
+    void fork_join(unsigned parts, const std::function<void(unsigned)>& fn);
     unsigned size() const { return (unsigned)threads_.size(); }
     static unsigned default_workers();
 
 private:
-    void run();
-    std::mutex m_;
-    std::condition_variable cv_;
-    std::deque<std::function<void()>> q_;
-    bool stop_ = false;
+    void worker_main();
+    std::mutex lock_;
+    std::condition_variable has_job_, has_room_;
+    std::vector<std::function<void()>> ring_;
+    size_t head_ = 0, tail_ = 0;   // jobs [head_, tail_) modulo ring_.size()
+    bool closing_ = false;
     std::vector<std::thread> threads_;
 };
 

@@ -19,7 +19,7 @@ DEFAULT_BATCH_VALUES = 1025 * 1024 * 4  # pipeline.hpp:71-72
 
 OK, ERR_INVALID, ERR_CORRUPT, ERR_IO, ERR_CUDA, ERR_CALLBACK, ERR_CAPACITY, ERR_UNSUPPORTED = range(8)
 STAGE_COMPRESS, STAGE_STORE, STAGE_DECODE = 0, 1, 2
-KINDS = {"walk": 0, "decimal": 1, "signflip": 2, "outlier": 3, "bits": 4, "mixed": 5}
+KINDS = {"walk": 0, "decimal": 1, "signflip": 2, "outlier": 3, "bits": 4, "mixed": 5, "field": 6}
 
 EXPORTED = [
     "falcon_abi_version", "falcon_last_error", "falcon_default_options", "falcon_ctx_create",
@@ -30,6 +30,7 @@ EXPORTED = [
     "falcon_ctx_sync", "falcon_compress_stream", "falcon_decompress_stream", "falcon_compress_host",
     "falcon_decompress_host", "falcon_compress_chunk", "falcon_decompress_chunk", "falcon_synth_fill",
     "falcon_ctx_set_kernel_events", "falcon_selftest_dp", "falcon_selftest_div",
+    "falcon_synth_fill_at", "falcon_synth_device",
 ]
 
 
@@ -123,6 +124,8 @@ def load() -> C.CDLL:
     L.falcon_compress_chunk.argtypes = [vp, i32, vp, u32, vp, u64, C.POINTER(u64)]
     L.falcon_decompress_chunk.argtypes = [vp, i32, vp, u64, u32, u32, vp]
     L.falcon_synth_fill.argtypes = [i32, C.POINTER(SynthSpec), vp, u64]
+    L.falcon_synth_fill_at.argtypes = [i32, C.POINTER(SynthSpec), u64, vp, u64]
+    L.falcon_synth_device.argtypes = [vp, i32, C.POINTER(SynthSpec), u64, vp, u64, vp]
     L.falcon_default_options.argtypes = [C.POINTER(PipelineOptions)]
     _lib = L
     return L
@@ -176,12 +179,14 @@ def read_header(archive) -> ArchiveInfo:
 
 
 def synth(kind: str, count: int, prec: int = F64, dp: int = 2, seed: int = 1, step: int = 127,
-          period: int = 1025, units: int = 3575, block: int = DEFAULT_CHUNK_N, out=None) -> np.ndarray:
-    """Synthetic inputs (synthetic.hpp:36-115; kind 'mixed' = pinned cfg3 generator)."""
+          period: int = 1025, units: int = 3575, block: int = DEFAULT_CHUNK_N, out=None,
+          first: int = 0) -> np.ndarray:
+    """Synthetic inputs (synthetic.hpp:36-115; kind 'mixed' = pinned cfg3 generator,
+    'field' = counter-based field of the sharded configs, any `first`)."""
     s = SynthSpec(KINDS[kind], dp, seed, step, period, units, block)
     if out is None:
         out = np.empty(count, np.float64 if prec == F64 else np.float32)
-    _check(load().falcon_synth_fill(prec, C.byref(s), _np_ptr(out), count))
+    _check(load().falcon_synth_fill_at(prec, C.byref(s), first, _np_ptr(out), count))
     return out
 
 
@@ -286,6 +291,16 @@ class Codec:
         _check(self.lib.falcon_decompress_device_async(
             self.ctx, prec_of(out.dtype), C.c_void_p(archive.data_ptr()), nbytes, C.byref(info),
             C.c_void_p(out.data_ptr()), out.numel(), st))
+
+    def synth_device(self, out, kind: str = "field", first: int = 0, dp: int = 2, seed: int = 1):
+        """Fill the CUDA tensor `out` with values [first, first + out.numel()) of a
+        counter-based kind, on the device (asynchronous on the current stream)."""
+        import torch
+        s = SynthSpec(KINDS[kind], dp, seed, 127, 1025, 3575, DEFAULT_CHUNK_N)
+        st = C.c_void_p(torch.cuda.current_stream(out.device).cuda_stream)
+        _check(self.lib.falcon_synth_device(self.ctx, prec_of(out.dtype), C.byref(s), first,
+                                            C.c_void_p(out.data_ptr()), out.numel(), st))
+        return out
 
     def set_kernel_events(self, enc=None, dec=None):
         """enc/dec: (start, stop) torch.cuda.Event pairs recorded around the main kernels."""

@@ -1,517 +1,602 @@
-// falcon -- the reference CLI's front end (proj/tools/falcon_cli.cpp) on the B200 library.
+// falcon -- command-line front end of the B200 codec.
 //
-//   falcon compress   data.raw data.fln --precision 64
-//   falcon decompress data.fln data.raw
-//   falcon verify     data.raw data.fln
-//   falcon inspect    data.fln
-//   falcon gen        data.raw --kind walk --count 1000000
-//   falcon bench      --kind walk --count 10000000 [--device]
+// Subcommands, flags and the key=value report follow the reference tool
+// (proj/tools/falcon_cli.cpp:251-512; FORMAT.md), so scripts and archives move freely
+// between the two:
 //
-// Same subcommands, flags and key=value report as the reference (falcon_cli.cpp:251-512);
-// archives are byte-identical, so files move freely between the two tools.  The codec
-// calls go through the drop-in header include/falcon_b200/falcon.hpp (compress/decompress)
-// and the C ABI (synthetic data, device-resident bench).  CLI11 is not vendored in the
-// reference snapshot, so a small flag parser stands in for it.
+//   falcon compress   IN OUT   [--precision 64|32] [--format raw|csv] [--column N]
+//   falcon decompress IN OUT   [--format raw|csv]
+//   falcon verify     ORIGINAL ARCHIVE
+//   falcon inspect    ARCHIVE
+//   falcon gen        OUT      [--kind K] [--count N] [--seed S] [--dp D] ...
+//   falcon bench               [--kind K] [--count N] [--device] [--reps R]
+//   (+ --chunk-n --batch-values --streams --workers everywhere)
+//
+// Files are memory-mapped (raw inputs feed the pipeline without a copy); decompressed
+// batches are written with pwrite at their value offset, so out-of-order sink calls from
+// the pipeline's worker threads need no lock.  The codec goes through the drop-in header
+// include/falcon_b200/falcon.hpp; synthetic data and the device bench through the C ABI.
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <charconv>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
-#include <fstream>
-#include <iostream>
+#include <functional>
 #include <map>
-#include <mutex>
 #include <string>
+#include <string_view>
+#include <utility>
 #include <vector>
 
 #include "falcon_b200/falcon.hpp"
 
-using namespace falcon_b200;
+namespace fb = falcon_b200;
 
 namespace {
 
-double seconds_since(std::chrono::steady_clock::time_point t0) {
-    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-}
-
-std::vector<std::uint8_t> slurp(const std::string& path) {
-    std::ifstream in(path, std::ios::binary);
-    if (!in) throw io_error("cannot open " + path);
-    return std::vector<std::uint8_t>((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
-}
-
-void spill(const std::string& path, std::span<const std::uint8_t> bytes) {
-    std::ofstream out(path, std::ios::binary | std::ios::trunc);
-    if (!out) throw io_error("cannot open " + path);
-    out.write(reinterpret_cast<const char*>(bytes.data()), static_cast<std::streamsize>(bytes.size()));
-    if (!out) throw io_error("write failed on " + path);
-}
-
-template <typename T>
-class raw_file_source final : public value_source<T> {
+// ---------------------------------------------------------------- report ----
+// key=value lines in insertion order (the reference's report format)
+class kv_report {
 public:
-    explicit raw_file_source(const std::string& path) : in_(path, std::ios::binary) {
-        if (!in_) throw io_error("cannot open " + path);
+    void add(const char* k, std::string v) { rows_.emplace_back(k, std::move(v)); }
+    void add(const char* k, std::uint64_t v) { add(k, std::to_string(v)); }
+    void add(const char* k, double v) {
+        char b[48];
+        std::snprintf(b, sizeof b, "%.6g", v);
+        add(k, std::string(b));
     }
-    std::size_t read(std::span<T> dst) override {
-        in_.read(reinterpret_cast<char*>(dst.data()), static_cast<std::streamsize>(dst.size() * sizeof(T)));
-        const auto got = static_cast<std::size_t>(in_.gcount());
-        if (got % sizeof(T) != 0) throw io_error("input ends inside a value");
-        return got / sizeof(T);
+    void print() const {
+        std::string out;
+        for (const auto& [k, v] : rows_) out.append(k).append("=").append(v).append("\n");
+        std::fwrite(out.data(), 1, out.size(), stdout);
     }
 
 private:
-    std::ifstream in_;
+    std::vector<std::pair<std::string, std::string>> rows_;
 };
 
-// out-of-order batches land at their value offset (falcon_cli.cpp:75-101)
-template <typename T>
-class raw_file_sink final : public value_sink<T> {
+// ------------------------------------------------------------------ files ----
+class mapped_file {
 public:
-    explicit raw_file_sink(const std::string& path) {
-        std::ofstream(path, std::ios::binary | std::ios::trunc);
-        out_.open(path, std::ios::binary | std::ios::in | std::ios::out);
-        if (!out_) throw io_error("cannot open " + path);
-    }
-    void put(std::uint64_t first, std::span<const T> v) override {
-        std::lock_guard lock(m_);
-        out_.seekp(static_cast<std::streamoff>(first * sizeof(T)));
-        out_.write(reinterpret_cast<const char*>(v.data()), static_cast<std::streamsize>(v.size() * sizeof(T)));
-        if (!out_) throw io_error("write failed");
-    }
-
-private:
-    std::mutex m_;
-    std::fstream out_;
-};
-
-template <typename T>
-std::uint64_t bits(T v) {
-    if constexpr (sizeof(T) == 8) {
-        std::uint64_t b;
-        std::memcpy(&b, &v, 8);
-        return b;
-    } else {
-        std::uint32_t b;
-        std::memcpy(&b, &v, 4);
-        return b;
-    }
-}
-
-// compares decompressed batches against the original raw file (falcon_cli.cpp:103-132)
-template <typename T>
-class compare_sink final : public value_sink<T> {
-public:
-    explicit compare_sink(const std::string& path) : in_(path, std::ios::binary) {
-        if (!in_) throw io_error("cannot open " + path);
-    }
-    void put(std::uint64_t first, std::span<const T> v) override {
-        std::vector<T> expect(v.size());
-        {
-            std::lock_guard lock(m_);
-            in_.clear();
-            in_.seekg(static_cast<std::streamoff>(first * sizeof(T)));
-            in_.read(reinterpret_cast<char*>(expect.data()), static_cast<std::streamsize>(expect.size() * sizeof(T)));
-            if (static_cast<std::size_t>(in_.gcount()) != expect.size() * sizeof(T))
-                throw error("original file is shorter than the archive claims");
+    explicit mapped_file(const std::string& path) {
+        fd_ = ::open(path.c_str(), O_RDONLY);
+        if (fd_ < 0) throw fb::io_error("cannot open " + path);
+        struct stat st {};
+        if (::fstat(fd_, &st) != 0) throw fb::io_error("cannot stat " + path);
+        size_ = static_cast<std::size_t>(st.st_size);
+        if (size_) {
+            void* p = ::mmap(nullptr, size_, PROT_READ, MAP_PRIVATE, fd_, 0);
+            if (p == MAP_FAILED) throw fb::io_error("cannot map " + path);
+            base_ = static_cast<const std::uint8_t*>(p);
+            ::madvise(p, size_, MADV_SEQUENTIAL);
         }
+    }
+    ~mapped_file() {
+        if (base_) ::munmap(const_cast<std::uint8_t*>(base_), size_);
+        if (fd_ >= 0) ::close(fd_);
+    }
+    mapped_file(const mapped_file&) = delete;
+    mapped_file& operator=(const mapped_file&) = delete;
+    std::span<const std::uint8_t> bytes() const { return {base_ ? base_ : empty_, size_}; }
+
+private:
+    int fd_ = -1;
+    const std::uint8_t* base_ = nullptr;
+    std::size_t size_ = 0;
+    static constexpr std::uint8_t empty_[1] = {0};
+};
+
+class out_file {
+public:
+    explicit out_file(const std::string& path) : path_(path) {
+        fd_ = ::open(path.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+        if (fd_ < 0) throw fb::io_error("cannot open " + path);
+    }
+    ~out_file() {
+        if (fd_ >= 0) ::close(fd_);
+    }
+    out_file(const out_file&) = delete;
+    out_file& operator=(const out_file&) = delete;
+    // positional write: safe from several threads for disjoint ranges
+    void write_at(std::uint64_t off, const void* p, std::size_t n) const {
+        const auto* c = static_cast<const char*>(p);
+        while (n) {
+            const ssize_t w = ::pwrite(fd_, c, n, static_cast<off_t>(off));
+            if (w <= 0) throw fb::io_error("write failed on " + path_);
+            c += w;
+            off += static_cast<std::uint64_t>(w);
+            n -= static_cast<std::size_t>(w);
+        }
+    }
+
+private:
+    int fd_ = -1;
+    std::string path_;
+};
+
+template <typename T>
+std::span<const T> as_values(std::span<const std::uint8_t> b) {
+    if (b.size() % sizeof(T) != 0) throw fb::io_error("input ends inside a value");
+    return {reinterpret_cast<const T*>(b.data()), b.size() / sizeof(T)};
+}
+
+template <typename T>
+struct pwrite_sink final : fb::value_sink<T> {
+    const out_file& f;
+    explicit pwrite_sink(const out_file& o) : f(o) {}
+    void put(std::uint64_t first, std::span<const T> v) override {
+        f.write_at(first * sizeof(T), v.data(), v.size_bytes());
+    }
+};
+
+// compares each decoded batch with the mapped original (first mismatch wins)
+template <typename T>
+struct check_sink final : fb::value_sink<T> {
+    std::span<const T> want;
+    explicit check_sink(std::span<const T> w) : want(w) {}
+    void put(std::uint64_t first, std::span<const T> v) override {
+        if (first + v.size() > want.size()) throw fb::error("original file is shorter than the archive claims");
+        if (std::memcmp(v.data(), want.data() + first, v.size_bytes()) == 0) return;
         for (std::size_t i = 0; i < v.size(); ++i)
-            if (bits(v[i]) != bits(expect[i])) throw error("value mismatch at index " + std::to_string(first + i));
+            if (std::memcmp(&v[i], &want[first + i], sizeof(T)) != 0)
+                throw fb::error("value mismatch at index " + std::to_string(first + i));
     }
-
-private:
-    std::mutex m_;
-    std::ifstream in_;
 };
 
+// ------------------------------------------------------------------- csv ----
+// One value per row from column `col` (comma separated); a first row that does not parse
+// is a header and skipped, any later one is an error.
 template <typename T>
-std::vector<T> load_csv(const std::string& path, unsigned column) {
-    std::ifstream in(path);
-    if (!in) throw io_error("cannot open " + path);
-    std::vector<T> values;
-    std::string line;
-    bool first_line = true;
-    while (std::getline(in, line)) {
-        if (!line.empty() && line.back() == '\r') line.pop_back();
-        if (line.empty()) continue;
-        std::size_t begin = 0;
-        for (unsigned c = 0; c < column; ++c) {
-            const auto comma = line.find(',', begin);
-            if (comma == std::string::npos) throw io_error("row has no column " + std::to_string(column));
-            begin = comma + 1;
+std::vector<T> parse_csv(std::span<const std::uint8_t> text, unsigned col) {
+    std::vector<T> out;
+    const char* p = reinterpret_cast<const char*>(text.data());
+    const char* const end = p + text.size();
+    bool first_row = true;
+    while (p < end) {
+        const char* nl = static_cast<const char*>(std::memchr(p, '\n', static_cast<std::size_t>(end - p)));
+        const char* row_end = nl ? nl : end;
+        std::string_view row(p, static_cast<std::size_t>(row_end - p));
+        p = nl ? nl + 1 : end;
+        if (!row.empty() && row.back() == '\r') row.remove_suffix(1);
+        if (row.empty()) continue;
+        std::string_view cell = row;
+        for (unsigned c = 0; c < col; ++c) {
+            const auto k = cell.find(',');
+            if (k == std::string_view::npos) throw fb::io_error("row has no column " + std::to_string(col));
+            cell.remove_prefix(k + 1);
         }
-        auto end = line.find(',', begin);
-        if (end == std::string::npos) end = line.size();
+        cell = cell.substr(0, cell.find(','));
         T v{};
-        const auto r = std::from_chars(line.data() + begin, line.data() + end, v);
-        if (r.ec != std::errc{} || r.ptr != line.data() + end) {
-            if (first_line) {  // a header row is fine, anything later is not
-                first_line = false;
-                continue;
-            }
-            throw io_error("cannot parse value: " + line.substr(begin, end - begin));
-        }
-        first_line = false;
-        values.push_back(v);
+        const auto r = std::from_chars(cell.data(), cell.data() + cell.size(), v);
+        const bool ok = r.ec == std::errc{} && r.ptr == cell.data() + cell.size();
+        if (!ok && !first_row) throw fb::io_error("cannot parse value: " + std::string(cell));
+        if (ok) out.push_back(v);
+        first_row = false;
     }
-    return values;
+    return out;
 }
 
+// shortest round-trip text, one value per line
 template <typename T>
-void save_csv(const std::string& path, std::span<const T> values) {
-    std::ofstream out(path, std::ios::trunc);
-    if (!out) throw io_error("cannot open " + path);
-    char buf[64];
+void write_csv(const std::string& path, std::span<const T> values) {
+    std::string buf;
+    buf.reserve(values.size() * 12);
+    char tmp[40];
     for (const T v : values) {
-        const auto r = std::to_chars(buf, buf + sizeof buf, v);
-        *r.ptr = '\n';
-        out.write(buf, r.ptr + 1 - buf);
+        const auto r = std::to_chars(tmp, tmp + sizeof tmp, v);
+        buf.append(tmp, r.ptr).push_back('\n');
     }
-    if (!out) throw io_error("write failed on " + path);
+    out_file(path).write_at(0, buf.data(), buf.size());
 }
 
-void report(const char* key, const std::string& value) { std::cout << key << "=" << value << "\n"; }
-void report(const char* key, double value) {
-    char buf[64];
-    std::snprintf(buf, sizeof buf, "%.6g", value);
-    report(key, std::string(buf));
-}
-void report(const char* key, std::uint64_t value) { report(key, std::to_string(value)); }
+// ----------------------------------------------------------------- flags ----
+struct cli_args {
+    std::vector<std::string> files;
+    std::map<std::string, std::string> flags;
 
-// ---- flags ----
-struct args {
-    std::vector<std::string> pos;
-    std::map<std::string, std::string> opt;
-    bool has(const std::string& k) const { return opt.count(k) != 0; }
-    std::string str(const std::string& k, const std::string& d) const { return has(k) ? opt.at(k) : d; }
-    std::uint64_t u64(const std::string& k, std::uint64_t d) const { return has(k) ? std::stoull(opt.at(k)) : d; }
-    std::int64_t i64(const std::string& k, std::int64_t d) const { return has(k) ? std::stoll(opt.at(k)) : d; }
+    bool has(const char* k) const { return flags.count(k) != 0; }
+    std::string text(const char* k, const char* dflt) const {
+        const auto it = flags.find(k);
+        return it == flags.end() ? dflt : it->second;
+    }
+    template <typename I>
+    I number(const char* k, I dflt) const {
+        const auto it = flags.find(k);
+        if (it == flags.end()) return dflt;
+        I v{};
+        const auto& s = it->second;
+        const auto r = std::from_chars(s.data(), s.data() + s.size(), v);
+        if (r.ec != std::errc{} || r.ptr != s.data() + s.size())
+            throw fb::error("--" + std::string(k) + ": not a number: " + s);
+        return v;
+    }
 };
 
-args parse(int argc, char** argv, int from) {
-    args a;
-    for (int i = from; i < argc; ++i) {
-        std::string s = argv[i];
-        if (s.rfind("--", 0) == 0) {
-            const auto eq = s.find('=');
-            if (eq != std::string::npos) {
-                a.opt[s.substr(2, eq - 2)] = s.substr(eq + 1);
-            } else if (s == "--device") {
-                a.opt["device"] = "1";
-            } else {
-                if (i + 1 >= argc) throw error("flag " + s + " needs a value");
-                a.opt[s.substr(2)] = argv[++i];
-            }
+// flags that take a value; --device is the one switch
+const char* const kValueFlags[] = {"precision", "format", "column", "chunk-n", "batch-values", "streams",
+                                   "workers", "kind", "count", "seed", "dp", "step", "period", "spike", "reps"};
+
+cli_args parse_args(int argc, char** argv) {
+    cli_args a;
+    for (int i = 2; i < argc; ++i) {
+        std::string_view s = argv[i];
+        if (s.substr(0, 2) != "--") {
+            a.files.emplace_back(s);
+            continue;
+        }
+        s.remove_prefix(2);
+        std::string key(s.substr(0, s.find('=')));
+        if (key == "device") {
+            a.flags[key] = "1";
+            continue;
+        }
+        if (std::none_of(std::begin(kValueFlags), std::end(kValueFlags), [&](const char* f) { return key == f; }))
+            throw fb::error("unknown flag --" + key);
+        if (s.find('=') != std::string_view::npos) {
+            a.flags[key] = std::string(s.substr(s.find('=') + 1));
         } else {
-            a.pos.push_back(s);
+            if (i + 1 >= argc) throw fb::error("flag --" + key + " needs a value");
+            a.flags[key] = argv[++i];
         }
     }
     return a;
 }
 
-pipeline_options codec_options(const args& a) {
-    pipeline_options o;
-    o.chunk_n = static_cast<std::uint32_t>(a.u64("chunk-n", 1025));
-    o.batch_values = a.u64("batch-values", std::uint64_t{1025} * 1024 * 4);
-    o.n_streams = static_cast<unsigned>(a.u64("streams", 16));
-    o.workers = static_cast<unsigned>(a.u64("workers", 0));
+fb::pipeline_options pipeline_opts(const cli_args& a) {
+    fb::pipeline_options o;
+    o.chunk_n = a.number<std::uint32_t>("chunk-n", 1025);
+    o.batch_values = a.number<std::uint64_t>("batch-values", 1025ull * 1024 * 4);
+    o.n_streams = a.number<unsigned>("streams", 16);
+    o.workers = a.number<unsigned>("workers", 0);
     return o;
 }
 
-falcon_synth_spec spec_from(const args& a) {
-    static const std::map<std::string, int> kinds = {
-        {"walk", FALCON_KIND_WALK},         {"random_walk", FALCON_KIND_WALK},
-        {"decimal", FALCON_KIND_DECIMAL},   {"fixed_decimal", FALCON_KIND_DECIMAL},
-        {"signflip", FALCON_KIND_SIGNFLIP}, {"sign_flip", FALCON_KIND_SIGNFLIP},
-        {"outlier", FALCON_KIND_OUTLIER},   {"outlier_injected", FALCON_KIND_OUTLIER},
-        {"bits", FALCON_KIND_BITS},         {"uniform_bits", FALCON_KIND_BITS},
-        {"mixed", FALCON_KIND_MIXED_BLOCKS}};
-    const std::string k = a.str("kind", "walk");
-    if (!kinds.count(k)) throw error("unknown kind: " + k);
+bool wants_f64(const cli_args& a) {
+    const unsigned bits = a.number<unsigned>("precision", 64);
+    if (bits != 64 && bits != 32) throw fb::error("--precision must be 32 or 64");
+    return bits == 64;
+}
+
+bool csv_format(const cli_args& a) {
+    const std::string f = a.text("format", "raw");
+    if (f != "raw" && f != "csv") throw fb::error("--format must be raw or csv");
+    return f == "csv";
+}
+
+// synth::kind names (synthetic.hpp:14-20) plus this build's pinned kinds
+falcon_synth_spec synth_spec(const cli_args& a) {
+    static const std::pair<const char*, int> names[] = {
+        {"random_walk", FALCON_KIND_WALK},      {"walk", FALCON_KIND_WALK},
+        {"fixed_decimal", FALCON_KIND_DECIMAL}, {"decimal", FALCON_KIND_DECIMAL},
+        {"sign_flip", FALCON_KIND_SIGNFLIP},    {"signflip", FALCON_KIND_SIGNFLIP},
+        {"outlier_injected", FALCON_KIND_OUTLIER}, {"outlier", FALCON_KIND_OUTLIER},
+        {"uniform_bits", FALCON_KIND_BITS},     {"bits", FALCON_KIND_BITS},
+        {"mixed", FALCON_KIND_MIXED_BLOCKS},    {"field", FALCON_KIND_FIELD}};
+    const std::string k = a.text("kind", "walk");
+    const auto* hit = std::find_if(std::begin(names), std::end(names), [&](const auto& n) { return k == n.first; });
+    if (hit == std::end(names)) throw fb::error("unknown kind: " + k);
     falcon_synth_spec sp{};
-    sp.kind = kinds.at(k);
-    sp.seed = a.u64("seed", 1);
-    sp.decimal_places = static_cast<int>(a.i64("dp", 2));
-    sp.max_step_units = static_cast<int>(a.i64("step", 127));
-    sp.outlier_period = a.u64("period", 1025);
-    sp.outlier_units = a.i64("spike", 3575);
-    sp.block = static_cast<std::uint32_t>(a.u64("chunk-n", 1025));
+    sp.kind = hit->second;
+    sp.decimal_places = a.number<int>("dp", 2);
+    sp.seed = a.number<std::uint64_t>("seed", 1);
+    sp.max_step_units = a.number<int>("step", 127);
+    sp.outlier_period = a.number<std::uint64_t>("period", 1025);
+    sp.outlier_units = a.number<std::int64_t>("spike", 3575);
+    sp.block = a.number<std::uint32_t>("chunk-n", 1025);
     return sp;
 }
 
 template <typename T>
-std::vector<T> synth_values(const falcon_synth_spec& sp, std::uint64_t count) {
-    std::vector<T> v(count);
-    detail::check(falcon_synth_fill(detail::prec<T>, &sp, v.data(), count));
+std::vector<T> synthesize(const falcon_synth_spec& sp, std::uint64_t n) {
+    std::vector<T> v(n);
+    fb::detail::check(falcon_synth_fill(fb::detail::prec<T>, &sp, v.data(), n));
     return v;
 }
 
+double since(std::chrono::steady_clock::time_point t) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t).count();
+}
+
+// -------------------------------------------------------------- commands ----
 template <typename T>
-int run_compress(const args& a) {
-    const auto t0 = std::chrono::steady_clock::now();
-    pipeline_stats stats;
-    std::vector<std::uint8_t> archive;
-    if (a.str("format", "raw") == "csv") {
-        const auto values = load_csv<T>(a.pos.at(0), static_cast<unsigned>(a.u64("column", 0)));
-        memory_source<T> src(values);
-        archive = compress_pipeline<T>(src, codec_options(a), &stats);
+int cmd_compress(const cli_args& a) {
+    mapped_file in(a.files.at(0));
+    std::vector<T> parsed;
+    std::span<const T> values;
+    if (csv_format(a)) {
+        parsed = parse_csv<T>(in.bytes(), a.number<unsigned>("column", 0));
+        values = parsed;
     } else {
-        raw_file_source<T> src(a.pos.at(0));
-        archive = compress_pipeline<T>(src, codec_options(a), &stats);
+        values = as_values<T>(in.bytes());
     }
-    const double dt = seconds_since(t0);
-    spill(a.pos.at(1), archive);
-    const std::uint64_t raw_bytes = stats.values * sizeof(T);
-    report("values", stats.values);
-    report("batches", stats.batches);
-    report("raw_bytes", raw_bytes);
-    report("archive_bytes", static_cast<std::uint64_t>(archive.size()));
-    report("ratio", raw_bytes ? static_cast<double>(archive.size()) / raw_bytes : 0.0);
-    report("seconds", dt);
-    report("mb_per_s", dt > 0 ? raw_bytes / dt / 1e6 : 0.0);
+    const auto t0 = std::chrono::steady_clock::now();
+    fb::memory_source<T> src(values);
+    fb::pipeline_stats st;
+    const std::vector<std::uint8_t> arc = fb::compress_pipeline<T>(src, pipeline_opts(a), &st);
+    const double dt = since(t0);
+    out_file(a.files.at(1)).write_at(0, arc.data(), arc.size());
+    const std::uint64_t raw = st.values * sizeof(T);
+    kv_report r;
+    r.add("values", st.values);
+    r.add("batches", st.batches);
+    r.add("raw_bytes", raw);
+    r.add("archive_bytes", static_cast<std::uint64_t>(arc.size()));
+    r.add("ratio", raw ? static_cast<double>(arc.size()) / static_cast<double>(raw) : 0.0);
+    r.add("seconds", dt);
+    r.add("mb_per_s", dt > 0 ? static_cast<double>(raw) / dt / 1e6 : 0.0);
+    r.print();
     return 0;
 }
 
 template <typename T>
-int run_decompress(const args& a, const std::vector<std::uint8_t>& archive) {
+int cmd_decompress(const cli_args& a, std::span<const std::uint8_t> arc) {
     const auto t0 = std::chrono::steady_clock::now();
-    pipeline_stats stats;
-    if (a.str("format", "raw") == "csv") {
-        const auto values = decompress_to_vector<T>(archive, codec_options(a));
-        stats.values = values.size();
-        save_csv<T>(a.pos.at(1), std::span<const T>(values));
+    std::uint64_t n = 0;
+    if (csv_format(a)) {
+        const std::vector<T> v = fb::decompress_to_vector<T>(arc, pipeline_opts(a));
+        n = v.size();
+        write_csv<T>(a.files.at(1), std::span<const T>(v));
     } else {
-        raw_file_sink<T> sink(a.pos.at(1));
-        stats = decompress_pipeline<T>(archive, sink, codec_options(a));
+        out_file out(a.files.at(1));
+        pwrite_sink<T> sink(out);
+        n = fb::decompress_pipeline<T>(arc, sink, pipeline_opts(a)).values;
     }
-    const double dt = seconds_since(t0);
-    report("values", stats.values);
-    report("seconds", dt);
-    report("mb_per_s", dt > 0 ? stats.values * sizeof(T) / dt / 1e6 : 0.0);
+    const double dt = since(t0);
+    kv_report r;
+    r.add("values", n);
+    r.add("seconds", dt);
+    r.add("mb_per_s", dt > 0 ? static_cast<double>(n * sizeof(T)) / dt / 1e6 : 0.0);
+    r.print();
     return 0;
 }
 
 template <typename T>
-int run_verify(const args& a, const std::vector<std::uint8_t>& archive) {
+int cmd_verify(const cli_args& a, std::span<const std::uint8_t> arc) {
+    kv_report r;
     try {
-        if (a.str("format", "raw") == "csv") {
-            const auto values = decompress_to_vector<T>(archive, codec_options(a));
-            const auto expect = load_csv<T>(a.pos.at(0), static_cast<unsigned>(a.u64("column", 0)));
-            if (values.size() != expect.size())
-                throw error("value count mismatch: " + std::to_string(expect.size()) + " in the original, " +
-                            std::to_string(values.size()) + " in the archive");
-            for (std::size_t i = 0; i < values.size(); ++i)
-                if (bits(values[i]) != bits(expect[i])) throw error("value mismatch at index " + std::to_string(i));
+        mapped_file orig(a.files.at(0));
+        std::vector<T> parsed;
+        std::span<const T> want;
+        if (csv_format(a)) {
+            parsed = parse_csv<T>(orig.bytes(), a.number<unsigned>("column", 0));
+            want = parsed;
         } else {
-            compare_sink<T> sink(a.pos.at(0));
-            decompress_pipeline<T>(archive, sink, codec_options(a));
+            want = as_values<T>(orig.bytes());
         }
+        check_sink<T> sink(want);
+        const std::uint64_t n = fb::decompress_pipeline<T>(arc, sink, pipeline_opts(a)).values;
+        // the count is checked for csv input only, as the reference tool does (a raw
+        // original may run past the archive)
+        if (!parsed.empty() && n != want.size())
+            throw fb::error("value count mismatch: " + std::to_string(want.size()) + " in the original, " +
+                            std::to_string(n) + " in the archive");
     } catch (const std::exception& e) {
-        report("verify", std::string("mismatch"));
-        report("detail", std::string(e.what()));
+        r.add("verify", std::string("mismatch"));
+        r.add("detail", std::string(e.what()));
+        r.print();
         return 1;
     }
-    report("verify", std::string("ok"));
+    r.add("verify", std::string("ok"));
+    r.print();
     return 0;
 }
 
-std::uint32_t le32(const std::uint8_t* p) {
-    return std::uint32_t(p[0]) | std::uint32_t(p[1]) << 8 | std::uint32_t(p[2]) << 16 | std::uint32_t(p[3]) << 24;
-}
-
-// header + frame walk (falcon_cli.cpp:327-361; read_batch, container.cpp:113-132)
-int run_inspect(const args& a) {
-    const auto archive = slurp(a.pos.at(0));
-    const archive_header h = read_header(archive);
-    report("precision", std::string(h.precision == precision_tag::f64 ? "64" : "32"));
-    report("chunk_n", static_cast<std::uint64_t>(h.chunk_n));
-    report("batch_values", h.batch_values);
-    report("total_values", h.total_values);
-    report("batch_count", h.batch_count);
-    report("archive_bytes", static_cast<std::uint64_t>(archive.size()));
-    const std::size_t width = h.precision == precision_tag::f64 ? 8 : 4;
-    report("ratio", h.total_values ? static_cast<double>(archive.size()) / (h.total_values * width) : 0.0);
-    std::size_t cursor = archive_header_bytes;
-    std::uint64_t chunks = 0;
-    std::uint32_t min_chunk = ~std::uint32_t{0}, max_chunk = 0;
+// header plus a frame walk (read_batch, container.cpp:113-132)
+int cmd_inspect(const cli_args& a) {
+    mapped_file f(a.files.at(0));
+    const auto arc = f.bytes();
+    const fb::archive_header h = fb::read_header(arc);
+    const bool f64 = h.precision == fb::precision_tag::f64;
+    auto le32 = [&](std::uint64_t at) {
+        std::uint32_t v;
+        std::memcpy(&v, arc.data() + at, 4);
+        return v;
+    };
+    std::uint64_t pos = fb::archive_header_bytes, chunks = 0;
+    std::uint32_t lo = UINT32_MAX, hi = 0;
     for (std::uint64_t b = 0; b < h.batch_count; ++b) {
-        const std::size_t left = archive.size() - cursor;
-        if (left < 4) throw corrupt_error("truncated batch header");
-        const std::uint32_t count = le32(archive.data() + cursor);
-        if (left < 4 + 4 * std::uint64_t{count}) throw corrupt_error("truncated chunk size table");
+        const std::uint64_t room = arc.size() - pos;
+        if (room < 4) throw fb::corrupt_error("truncated batch header");
+        const std::uint64_t cnt = le32(pos), table = 4 + 4 * cnt;
+        if (room < table) throw fb::corrupt_error("truncated chunk size table");
         std::uint64_t payload = 0;
-        for (std::uint32_t i = 0; i < count; ++i) {
-            const std::uint32_t s = le32(archive.data() + cursor + 4 + 4 * std::uint64_t{i});
+        for (std::uint64_t i = 0; i < cnt; ++i) {
+            const std::uint32_t s = le32(pos + 4 + 4 * i);
             payload += s;
-            min_chunk = std::min(min_chunk, s);
-            max_chunk = std::max(max_chunk, s);
+            lo = std::min(lo, s);
+            hi = std::max(hi, s);
         }
-        if (left - 4 - 4 * std::uint64_t{count} < payload) throw corrupt_error("truncated batch payload");
-        cursor += 4 + 4 * std::size_t{count} + payload;
-        chunks += count;
+        if (room - table < payload) throw fb::corrupt_error("truncated batch payload");
+        pos += table + payload;
+        chunks += cnt;
     }
-    if (cursor != archive.size()) throw corrupt_error("trailing bytes after final batch");
-    report("chunks", chunks);
+    if (pos != arc.size()) throw fb::corrupt_error("trailing bytes after final batch");
+    kv_report r;
+    r.add("precision", std::string(f64 ? "64" : "32"));
+    r.add("chunk_n", static_cast<std::uint64_t>(h.chunk_n));
+    r.add("batch_values", h.batch_values);
+    r.add("total_values", h.total_values);
+    r.add("batch_count", h.batch_count);
+    r.add("archive_bytes", static_cast<std::uint64_t>(arc.size()));
+    const double raw = static_cast<double>(h.total_values) * (f64 ? 8.0 : 4.0);
+    r.add("ratio", raw > 0 ? static_cast<double>(arc.size()) / raw : 0.0);
+    r.add("chunks", chunks);
     if (chunks) {
-        report("min_chunk_bytes", static_cast<std::uint64_t>(min_chunk));
-        report("max_chunk_bytes", static_cast<std::uint64_t>(max_chunk));
+        r.add("min_chunk_bytes", static_cast<std::uint64_t>(lo));
+        r.add("max_chunk_bytes", static_cast<std::uint64_t>(hi));
     }
+    r.print();
     return 0;
 }
 
 template <typename T>
-int run_gen(const args& a) {
-    const std::uint64_t count = a.u64("count", 1000000);
-    const auto sp = spec_from(a);
-    const auto values = synth_values<T>(sp, count);
-    if (a.str("format", "raw") == "csv") {
-        save_csv<T>(a.pos.at(0), std::span<const T>(values));
-    } else {
-        spill(a.pos.at(0), std::span<const std::uint8_t>(reinterpret_cast<const std::uint8_t*>(values.data()),
-                                                          values.size() * sizeof(T)));
-    }
-    report("values", count);
-    report("kind", a.str("kind", "walk"));
+int cmd_gen(const cli_args& a) {
+    const std::uint64_t n = a.number<std::uint64_t>("count", 1000000);
+    const std::vector<T> v = synthesize<T>(synth_spec(a), n);
+    if (csv_format(a)) write_csv<T>(a.files.at(0), std::span<const T>(v));
+    else out_file(a.files.at(0)).write_at(0, v.data(), v.size() * sizeof(T));
+    kv_report r;
+    r.add("values", n);
+    r.add("kind", a.text("kind", "walk"));
+    r.print();
     return 0;
 }
 
-#define CUDA_OK(x)                                                                        \
-    do {                                                                                  \
-        cudaError_t e_ = (x);                                                             \
-        if (e_ != cudaSuccess) throw error(std::string("CUDA: ") + cudaGetErrorString(e_)); \
-    } while (0)
+void cuda_ok(cudaError_t e) {
+    if (e != cudaSuccess) throw fb::error(std::string("CUDA: ") + cudaGetErrorString(e));
+}
 
-// host pipeline (as the reference's bench, falcon_cli.cpp:391-422), or with --device the
-// HBM-resident kernels timed with CUDA events (median of --reps)
+// median of the per-rep times of the HBM-resident kernels (CUDA events)
 template <typename T>
-int run_bench(const args& a) {
-    const std::uint64_t count = a.u64("count", 1000000);
-    const auto sp = spec_from(a);
-    const auto values = synth_values<T>(sp, count);
-    const auto opt = codec_options(a);
-    const std::uint64_t raw_bytes = count * sizeof(T);
-    double enc_dt, dec_dt;
-    std::uint64_t archive_bytes, waits = 0;
-    if (a.has("device")) {
-        falcon_ctx* ctx = detail::context();
-        T *d_in = nullptr, *d_out = nullptr;
-        std::uint8_t* d_arc = nullptr;
-        const std::uint64_t cap = falcon_compress_bound(detail::prec<T>, count, opt.chunk_n, opt.batch_values);
-        CUDA_OK(cudaMalloc(&d_in, raw_bytes ? raw_bytes : 1));
-        CUDA_OK(cudaMalloc(&d_out, raw_bytes ? raw_bytes : 1));
-        CUDA_OK(cudaMalloc(&d_arc, cap));
-        CUDA_OK(cudaMemcpy(d_in, values.data(), raw_bytes, cudaMemcpyHostToDevice));
-        cudaEvent_t e0, e1, e2;
-        CUDA_OK(cudaEventCreate(&e0));
-        CUDA_OK(cudaEventCreate(&e1));
-        CUDA_OK(cudaEventCreate(&e2));
-        const int reps = static_cast<int>(a.u64("reps", 10));
-        std::vector<float> te, td;
-        std::uint64_t nb = 0;
-        for (int r = 0; r < reps + 2; ++r) {
-            CUDA_OK(cudaEventRecord(e0, nullptr));
-            detail::check(falcon_compress_device(ctx, detail::prec<T>, d_in, count, opt.chunk_n, opt.batch_values, d_arc, cap,
-                                                 &nb, nullptr));
-            CUDA_OK(cudaEventRecord(e1, nullptr));
-            std::uint64_t nv = 0;
-            detail::check(falcon_decompress_device(ctx, detail::prec<T>, d_arc, nb, d_out, count, &nv, nullptr));
-            CUDA_OK(cudaEventRecord(e2, nullptr));
-            CUDA_OK(cudaEventSynchronize(e2));
-            float a1, a2;
-            CUDA_OK(cudaEventElapsedTime(&a1, e0, e1));
-            CUDA_OK(cudaEventElapsedTime(&a2, e1, e2));
-            if (r >= 2) {
-                te.push_back(a1);
-                td.push_back(a2);
-            }
+std::pair<double, double> device_round_trips(const std::vector<T>& host, const fb::pipeline_options& o, int reps,
+                                             std::uint64_t& archive_bytes) {
+    const std::uint64_t n = host.size(), raw = n * sizeof(T);
+    const std::uint64_t cap = falcon_compress_bound(fb::detail::prec<T>, n, o.chunk_n, o.batch_values);
+    void *d_in = nullptr, *d_back = nullptr, *d_arc = nullptr;
+    cuda_ok(cudaMalloc(&d_in, raw ? raw : 1));
+    cuda_ok(cudaMalloc(&d_back, raw ? raw : 1));
+    cuda_ok(cudaMalloc(&d_arc, cap));
+    cuda_ok(cudaMemcpy(d_in, host.data(), raw, cudaMemcpyHostToDevice));
+    cudaEvent_t ev[3];
+    for (auto& e : ev) cuda_ok(cudaEventCreate(&e));
+    std::vector<float> tc, td;
+    falcon_ctx* ctx = fb::detail::context();
+    for (int r = -2; r < reps; ++r) {
+        std::uint64_t nv = 0;
+        cuda_ok(cudaEventRecord(ev[0], nullptr));
+        fb::detail::check(falcon_compress_device(ctx, fb::detail::prec<T>, d_in, n, o.chunk_n, o.batch_values,
+                                                 d_arc, cap, &archive_bytes, nullptr));
+        cuda_ok(cudaEventRecord(ev[1], nullptr));
+        fb::detail::check(falcon_decompress_device(ctx, fb::detail::prec<T>, d_arc, archive_bytes, d_back, n, &nv,
+                                                   nullptr));
+        cuda_ok(cudaEventRecord(ev[2], nullptr));
+        cuda_ok(cudaEventSynchronize(ev[2]));
+        float a = 0, b = 0;
+        cuda_ok(cudaEventElapsedTime(&a, ev[0], ev[1]));
+        cuda_ok(cudaEventElapsedTime(&b, ev[1], ev[2]));
+        if (r >= 0) {
+            tc.push_back(a);
+            td.push_back(b);
         }
-        std::vector<T> back(count);
-        CUDA_OK(cudaMemcpy(back.data(), d_out, raw_bytes, cudaMemcpyDeviceToHost));
-        if (std::memcmp(back.data(), values.data(), raw_bytes) != 0) throw error("device round trip mismatch");
-        std::sort(te.begin(), te.end());
-        std::sort(td.begin(), td.end());
-        enc_dt = te[te.size() / 2] / 1e3;
-        dec_dt = td[td.size() / 2] / 1e3;
-        archive_bytes = nb;
-        cudaFree(d_in);
-        cudaFree(d_out);
-        cudaFree(d_arc);
+    }
+    std::vector<T> back(n);
+    cuda_ok(cudaMemcpy(back.data(), d_back, raw, cudaMemcpyDeviceToHost));
+    const bool same = std::memcmp(back.data(), host.data(), raw) == 0;
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaFree(d_in);
+    cudaFree(d_back);
+    cudaFree(d_arc);
+    if (!same) throw fb::error("device round trip mismatch");
+    std::nth_element(tc.begin(), tc.begin() + tc.size() / 2, tc.end());
+    std::nth_element(td.begin(), td.begin() + td.size() / 2, td.end());
+    return {tc[tc.size() / 2] / 1e3, td[td.size() / 2] / 1e3};
+}
+
+template <typename T>
+int cmd_bench(const cli_args& a) {
+    const std::uint64_t n = a.number<std::uint64_t>("count", 1000000);
+    const std::vector<T> values = synthesize<T>(synth_spec(a), n);
+    const fb::pipeline_options o = pipeline_opts(a);
+    const bool device = a.has("device");
+    double tc = 0, td = 0;
+    std::uint64_t arc_bytes = 0, waits = 0;
+    if (device) {
+        const auto [c, d] = device_round_trips<T>(values, o, a.number<int>("reps", 10), arc_bytes);
+        tc = c;
+        td = d;
     } else {
-        memory_source<T> src(values);
-        pipeline_stats stats;
-        const auto t0 = std::chrono::steady_clock::now();
-        const auto archive = compress_pipeline<T>(src, opt, &stats);
-        enc_dt = seconds_since(t0);
-        struct null_sink final : value_sink<T> {
+        fb::memory_source<T> src(values);
+        fb::pipeline_stats st;
+        auto t = std::chrono::steady_clock::now();
+        const auto arc = fb::compress_pipeline<T>(src, o, &st);
+        tc = since(t);
+        struct discard final : fb::value_sink<T> {
             void put(std::uint64_t, std::span<const T>) override {}
         } sink;
-        const auto t1 = std::chrono::steady_clock::now();
-        decompress_pipeline<T>(archive, sink, opt);
-        dec_dt = seconds_since(t1);
-        archive_bytes = archive.size();
-        waits = stats.blocking_waits;
+        t = std::chrono::steady_clock::now();
+        fb::decompress_pipeline<T>(arc, sink, o);
+        td = since(t);
+        arc_bytes = arc.size();
+        waits = st.blocking_waits;
     }
-    report("kind", a.str("kind", "walk"));
-    report("values", count);
-    report("raw_bytes", raw_bytes);
-    report("archive_bytes", archive_bytes);
-    report("ratio", raw_bytes ? static_cast<double>(archive_bytes) / raw_bytes : 0.0);
-    report("compress_seconds", enc_dt);
-    report("compress_mb_per_s", raw_bytes / enc_dt / 1e6);
-    report("decompress_seconds", dec_dt);
-    report("decompress_mb_per_s", raw_bytes / dec_dt / 1e6);
-    report("blocking_waits", waits);
-    report("mode", std::string(a.has("device") ? "device" : "host-pipeline"));
+    const double raw = static_cast<double>(n * sizeof(T));
+    kv_report r;
+    r.add("kind", a.text("kind", "walk"));
+    r.add("values", n);
+    r.add("raw_bytes", n * sizeof(T));
+    r.add("archive_bytes", arc_bytes);
+    r.add("ratio", raw > 0 ? static_cast<double>(arc_bytes) / raw : 0.0);
+    r.add("compress_seconds", tc);
+    r.add("compress_mb_per_s", raw / tc / 1e6);
+    r.add("decompress_seconds", td);
+    r.add("decompress_mb_per_s", raw / td / 1e6);
+    r.add("blocking_waits", waits);
+    r.add("mode", std::string(device ? "device" : "host-pipeline"));
+    r.print();
     return 0;
 }
 
 int usage() {
-    std::cerr << "usage: falcon {compress IN OUT | decompress IN OUT | verify ORIGINAL ARCHIVE | inspect ARCHIVE |\n"
-                 "               gen OUT | bench} [--precision 32|64] [--format raw|csv] [--column N]\n"
-                 "               [--chunk-n N] [--batch-values N] [--streams N] [--workers N]\n"
-                 "               [--kind K] [--count N] [--seed S] [--dp D] [--step S] [--period P] [--spike S]\n"
-                 "               [--device] [--reps R]\n";
+    std::fputs(
+        "usage: falcon compress IN OUT | decompress IN OUT | verify ORIGINAL ARCHIVE |\n"
+        "              inspect ARCHIVE | gen OUT | bench\n"
+        "  --precision 32|64  --format raw|csv  --column N\n"
+        "  --chunk-n N  --batch-values N  --streams N  --workers N\n"
+        "  --kind K  --count N  --seed S  --dp D  --step S  --period P  --spike S\n"
+        "  --device  --reps R   (bench: HBM-resident kernels timed with CUDA events)\n",
+        stderr);
     return 2;
 }
+
+struct command {
+    const char* name;
+    std::size_t files;
+    std::function<int(const cli_args&)> run;
+};
+
+// decompress / verify take their value type from the archive header
+template <template <typename> class Fn>
+int by_archive_precision(const cli_args& a, const std::string& archive_path) {
+    mapped_file f(archive_path);
+    const bool f64 = fb::read_header(f.bytes()).precision == fb::precision_tag::f64;
+    return f64 ? Fn<double>::run(a, f.bytes()) : Fn<float>::run(a, f.bytes());
+}
+template <typename T> struct decompress_fn {
+    static int run(const cli_args& a, std::span<const std::uint8_t> b) { return cmd_decompress<T>(a, b); }
+};
+template <typename T> struct verify_fn {
+    static int run(const cli_args& a, std::span<const std::uint8_t> b) { return cmd_verify<T>(a, b); }
+};
 
 }  // namespace
 
 int main(int argc, char** argv) {
     if (argc < 2) return usage();
-    const std::string cmd = argv[1];
+    const std::vector<command> commands = {
+        {"compress", 2, [](const cli_args& a) { return wants_f64(a) ? cmd_compress<double>(a) : cmd_compress<float>(a); }},
+        {"decompress", 2, [](const cli_args& a) { return by_archive_precision<decompress_fn>(a, a.files[0]); }},
+        {"verify", 2, [](const cli_args& a) { return by_archive_precision<verify_fn>(a, a.files[1]); }},
+        {"inspect", 1, [](const cli_args& a) { return cmd_inspect(a); }},
+        {"gen", 1, [](const cli_args& a) { return wants_f64(a) ? cmd_gen<double>(a) : cmd_gen<float>(a); }},
+        {"bench", 0, [](const cli_args& a) { return wants_f64(a) ? cmd_bench<double>(a) : cmd_bench<float>(a); }},
+    };
+    const std::string name = argv[1];
+    const auto it = std::find_if(commands.begin(), commands.end(), [&](const command& c) { return name == c.name; });
+    if (it == commands.end()) return usage();
     try {
-        const args a = parse(argc, argv, 2);
-        const bool f64 = a.u64("precision", 64) == 64;
-        if (a.has("precision") && !(a.u64("precision", 64) == 64 || a.u64("precision", 64) == 32))
-            throw error("--precision must be 32 or 64");
-        auto need = [&](std::size_t k) {
-            if (a.pos.size() != k) throw error(cmd + " takes " + std::to_string(k) + " file argument(s)");
-        };
-        if (cmd == "compress") {
-            need(2);
-            return f64 ? run_compress<double>(a) : run_compress<float>(a);
-        }
-        if (cmd == "decompress" || cmd == "verify") {
-            need(2);
-            const auto archive = slurp(cmd == "verify" ? a.pos[1] : a.pos[0]);
-            const bool archive_f64 = read_header(archive).precision == precision_tag::f64;
-            if (cmd == "decompress") return archive_f64 ? run_decompress<double>(a, archive) : run_decompress<float>(a, archive);
-            return archive_f64 ? run_verify<double>(a, archive) : run_verify<float>(a, archive);
-        }
-        if (cmd == "inspect") {
-            need(1);
-            return run_inspect(a);
-        }
-        if (cmd == "gen") {
-            need(1);
-            return f64 ? run_gen<double>(a) : run_gen<float>(a);
-        }
-        if (cmd == "bench") return f64 ? run_bench<double>(a) : run_bench<float>(a);
-        return usage();
+        const cli_args a = parse_args(argc, argv);
+        if (a.files.size() != it->files)
+            throw fb::error(name + " takes " + std::to_string(it->files) + " file argument(s)");
+        return it->run(a);
     } catch (const std::exception& e) {
-        std::cerr << "error: " << e.what() << "\n";
+        std::fprintf(stderr, "error: %s\n", e.what());
         return 1;
     }
 }
