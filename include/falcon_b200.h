@@ -192,6 +192,25 @@ falcon_status falcon_decompress_host(falcon_ctx* ctx, int precision, const uint8
                                      uint64_t* n_values, const falcon_pipeline_options* opt,
                                      falcon_pipeline_stats* stats);
 
+/* ---- host-resident across several GPUs ("a device list") ----
+ * ctxs[0..n_ctx): one context per GPU.  Batches are split into contiguous ranges, one per
+ * context (batch frames are context-free, container.cpp:88-111); each GPU runs its own
+ * multi-stream pipeline concurrently (one host thread per context) and the frames are
+ * concatenated in batch order after the one 47-byte header.  The archive bytes equal
+ * falcon_compress_host's for any n_ctx.  Decompress locates the frames once on the host
+ * (size tables only), then every GPU decodes its batch range into its value range.
+ * Errors: the lowest-numbered failing context's status and message. */
+falcon_status falcon_compress_host_multi(falcon_ctx* const* ctxs, unsigned n_ctx, int precision,
+                                         const void* values, uint64_t n_values,
+                                         const falcon_pipeline_options* opt, uint8_t* out,
+                                         uint64_t out_cap, uint64_t* out_bytes,
+                                         falcon_pipeline_stats* stats);
+falcon_status falcon_decompress_host_multi(falcon_ctx* const* ctxs, unsigned n_ctx, int precision,
+                                           const uint8_t* archive, uint64_t archive_bytes,
+                                           void* values, uint64_t cap_values, uint64_t* n_values,
+                                           const falcon_pipeline_options* opt,
+                                           falcon_pipeline_stats* stats);
+
 /* ---- per-chunk operators (GPU-backed; host buffers) ---- */
 /* Encodes exactly chunk_n values; returns the encoded length in *out_len. */
 falcon_status falcon_compress_chunk(falcon_ctx* ctx, int precision, const void* values,

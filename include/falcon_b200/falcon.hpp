@@ -8,7 +8,7 @@
 //   pipeline_options / pipeline_stats / stage_* ids           pipeline.hpp:66-85
 //   compress_pipeline<T>                                      pipeline.hpp:156-159
 //   decompress_pipeline<T>, decompress_to_vector<T>           pipeline.hpp:370-476
-//   compress_chunk<T>, decompress_chunk<T>                    chunk_codec.hpp:50-131
+//   chunk_workspace<T>, compress_chunk<T>, decompress_chunk<T> chunk_codec.hpp:43-131
 //   max_encoded_chunk_size<T>                                 chunk_codec.hpp:36-41
 //   archive_header, write_header, read_header                 container.hpp:12-27, container.cpp:44-86
 //   error / corrupt_error / io_error                          error.hpp:8-19
@@ -283,23 +283,51 @@ constexpr std::size_t max_encoded_chunk_size(std::size_t n) noexcept {
     return 3 + sizeof(T) + (sizeof(T) * 8 + 7) / 8 + sizeof(T) * 8 * ((n - 1) / 8);
 }
 
-// compress_chunk / decompress_chunk (chunk_codec.hpp:50-131), GPU-backed
+// chunk_workspace (chunk_codec.hpp:43-48): the reference keeps its lane and plane scratch
+// here so steady-state calls allocate nothing.  On the GPU the scratch (device input and
+// output buffers) lives in the library context and is reused across calls; the workspace
+// keeps a host staging vector for the encoded bytes.
 template <typename T>
-std::vector<std::uint8_t> compress_chunk(std::span<const T> values) {
-    std::vector<std::uint8_t> out(max_encoded_chunk_size<T>(values.size()));
+struct chunk_workspace {
+    std::vector<std::uint8_t> enc;
+};
+
+// compress_chunk (chunk_codec.hpp:50-74): appends the encoded chunk to `out`
+template <typename T>
+void compress_chunk(std::span<const T> values, chunk_workspace<T>& ws, std::vector<std::uint8_t>& out) {
+    ws.enc.resize(max_encoded_chunk_size<T>(values.size()));
     std::uint64_t len = 0;
     detail::check(falcon_compress_chunk(detail::context(), detail::prec<T>, values.data(),
-                                        static_cast<std::uint32_t>(values.size()), out.data(), out.size(), &len));
-    out.resize(len);
+                                        static_cast<std::uint32_t>(values.size()), ws.enc.data(), ws.enc.size(),
+                                        &len));
+    out.insert(out.end(), ws.enc.begin(), ws.enc.begin() + static_cast<std::ptrdiff_t>(len));
+}
+
+template <typename T>
+std::vector<std::uint8_t> compress_chunk(std::span<const T> values) {
+    chunk_workspace<T> ws;
+    std::vector<std::uint8_t> out;
+    compress_chunk<T>(values, ws, out);
     return out;
+}
+
+// decompress_chunk (chunk_codec.hpp:86-122): `in` spans exactly one encoded chunk; `out`
+// is resized to `count` values (the padded tail of a final chunk is dropped)
+template <typename T>
+void decompress_chunk(std::span<const std::uint8_t> in, std::size_t n, std::size_t count, chunk_workspace<T>&,
+                      std::vector<T>& out) {
+    if (count > n) throw error("decompress_chunk: count exceeds chunk capacity");
+    out.resize(count);
+    detail::check(falcon_decompress_chunk(detail::context(), detail::prec<T>, in.data(), in.size(),
+                                          static_cast<std::uint32_t>(n), static_cast<std::uint32_t>(count),
+                                          out.data()));
 }
 
 template <typename T>
 std::vector<T> decompress_chunk(std::span<const std::uint8_t> in, std::size_t n, std::size_t count) {
-    std::vector<T> out(count);
-    detail::check(falcon_decompress_chunk(detail::context(), detail::prec<T>, in.data(), in.size(),
-                                          static_cast<std::uint32_t>(n), static_cast<std::uint32_t>(count),
-                                          out.data()));
+    chunk_workspace<T> ws;
+    std::vector<T> out;
+    decompress_chunk<T>(in, n, count, ws, out);
     return out;
 }
 

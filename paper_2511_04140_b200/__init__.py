@@ -7,3 +7,4 @@ ctypes binding used by the tests and bench.
 from .falcon import (F32, F64, Codec, CorruptError, CudaError, FalconError, PipelineOptions,  # noqa: F401
                      PipelineStats, compress_bound, load, max_encoded_chunk_size, options,
                      read_header, synth)
+from .falcon import compress_host_multi, decompress_host_multi  # noqa: F401

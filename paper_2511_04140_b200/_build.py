@@ -58,7 +58,7 @@ def build(verbose: bool = False, force: bool = False, defines: tuple = (), out: 
                 print(out)
     if force or jobs or _mtime(lib) < max(_mtime(o) for o in objs):
         run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
-             "-o", lib, *objs, "-lpthread"])
+             "-o", lib, *objs, "-lpthread", "-ldl"])
     return lib
 
 

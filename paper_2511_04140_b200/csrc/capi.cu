@@ -222,6 +222,7 @@ falcon_status falcon_compress_device_async(falcon_ctx* ctx, int precision, const
                                            uint64_t n_values, uint32_t chunk_n,
                                            uint64_t batch_values, void* d_out, uint64_t out_cap,
                                            uint64_t* d_out_bytes, void* stream) {
+    FB_NVTX("falcon_compress_device_async");
     if (!ctx) return set_error(FALCON_ERR_INVALID, "null context");
     std::lock_guard<std::mutex> lock(ctx->api_mutex);
     device_guard dg(ctx->device);
@@ -234,6 +235,7 @@ falcon_status falcon_compress_device(falcon_ctx* ctx, int precision, const void*
                                      uint64_t n_values, uint32_t chunk_n, uint64_t batch_values,
                                      void* d_out, uint64_t out_cap, uint64_t* out_bytes,
                                      void* stream) {
+    FB_NVTX("falcon_compress_device");
     if (!ctx) return set_error(FALCON_ERR_INVALID, "null context");
     std::lock_guard<std::mutex> lock(ctx->api_mutex);
     device_guard dg(ctx->device);
@@ -257,6 +259,7 @@ falcon_status falcon_decompress_device_async(falcon_ctx* ctx, int precision,
                                              const void* d_archive, uint64_t archive_bytes,
                                              const falcon_archive_info* info, void* d_values,
                                              uint64_t cap_values, void* stream) {
+    FB_NVTX("falcon_decompress_device_async");
     if (!ctx || !info) return set_error(FALCON_ERR_INVALID, "null argument");
     std::lock_guard<std::mutex> lock(ctx->api_mutex);
     device_guard dg(ctx->device);
@@ -269,6 +272,7 @@ falcon_status falcon_decompress_device_chained(falcon_ctx* ctx, int precision, c
                                                const uint64_t* d_archive_bytes,
                                                const falcon_archive_info* info, void* d_values,
                                                uint64_t cap_values, void* stream) {
+    FB_NVTX("falcon_decompress_device_chained");
     if (!ctx || !info || !d_archive_bytes) return set_error(FALCON_ERR_INVALID, "null argument");
     std::lock_guard<std::mutex> lock(ctx->api_mutex);
     device_guard dg(ctx->device);
@@ -280,6 +284,7 @@ falcon_status falcon_decompress_device_chained(falcon_ctx* ctx, int precision, c
 falcon_status falcon_decompress_device(falcon_ctx* ctx, int precision, const void* d_archive,
                                        uint64_t archive_bytes, void* d_values,
                                        uint64_t cap_values, uint64_t* n_values, void* stream) {
+    FB_NVTX("falcon_decompress_device");
     if (!ctx) return set_error(FALCON_ERR_INVALID, "null context");
     std::lock_guard<std::mutex> lock(ctx->api_mutex);
     device_guard dg(ctx->device);
@@ -308,6 +313,7 @@ falcon_status falcon_decompress_device(falcon_ctx* ctx, int precision, const voi
 
 falcon_status falcon_archive_index(falcon_ctx* ctx, const void* d_archive, uint64_t archive_bytes,
                                    const falcon_archive_info* info, uint64_t* d_index, void* stream) {
+    FB_NVTX("falcon_archive_index");
     if (!ctx || !info || !d_index) return set_error(FALCON_ERR_INVALID, "null argument");
     std::lock_guard<std::mutex> lock(ctx->api_mutex);
     device_guard dg(ctx->device);
@@ -327,6 +333,7 @@ falcon_status falcon_decompress_device_range(falcon_ctx* ctx, int precision, con
                                              const falcon_archive_info* info, const uint64_t* index,
                                              uint64_t first_batch, uint64_t n_batches, void* d_values,
                                              uint64_t cap_values, uint64_t* n_values, void* stream) {
+    FB_NVTX("falcon_decompress_device_range");
     if (!ctx || !info || !index) return set_error(FALCON_ERR_INVALID, "null argument");
     if (first_batch > info->batch_count || n_batches > info->batch_count - first_batch)
         return set_error(FALCON_ERR_INVALID, "batch range outside the archive");
@@ -378,6 +385,7 @@ falcon_status falcon_ctx_set_kernel_events(falcon_ctx* ctx, void* enc_start, voi
 }
 
 falcon_status falcon_ctx_sync(falcon_ctx* ctx, void* stream) {
+    FB_NVTX("falcon_ctx_sync");
     if (!ctx) return set_error(FALCON_ERR_INVALID, "null context");
     std::lock_guard<std::mutex> lock(ctx->api_mutex);
     device_guard dg(ctx->device);
@@ -424,11 +432,15 @@ falcon_status falcon_selftest_div(falcon_ctx* ctx, int precision, const int64_t*
 falcon_status falcon_compress_chunk(falcon_ctx* ctx, int precision, const void* values,
                                     uint32_t chunk_n, uint8_t* out, uint64_t out_cap,
                                     uint64_t* out_len) {
+    FB_NVTX("falcon_compress_chunk");
     if (!ctx) return set_error(FALCON_ERR_INVALID, "null context");
     FB_TRY(validate_options(chunk_n, chunk_n));
     const size_t esz = lane_bytes(precision);
     const uint64_t bound = falcon_compress_bound(precision, chunk_n, chunk_n, chunk_n);
-    device_buffer din, dout;
+    // device scratch reused across calls (chunk_workspace, chunk_codec.hpp:43-48)
+    std::lock_guard<std::mutex> chunk_lock(ctx->chunk_mutex);
+    device_buffer& din = ctx->chunk_a;
+    device_buffer& dout = ctx->chunk_b;
     FB_TRY(din.ensure(chunk_n * esz));
     FB_TRY(dout.ensure(bound));
     {
@@ -451,6 +463,7 @@ falcon_status falcon_compress_chunk(falcon_ctx* ctx, int precision, const void* 
 
 falcon_status falcon_decompress_chunk(falcon_ctx* ctx, int precision, const uint8_t* in,
                                       uint64_t len, uint32_t chunk_n, uint32_t count, void* values) {
+    FB_NVTX("falcon_decompress_chunk");
     if (!ctx) return set_error(FALCON_ERR_INVALID, "null context");
     if (count > chunk_n)  // chunk_codec.hpp:92-93
         return set_error(FALCON_ERR_INVALID, "decompress_chunk: count exceeds chunk capacity");
@@ -465,7 +478,9 @@ falcon_status falcon_decompress_chunk(falcon_ctx* ctx, int precision, const uint
     std::memcpy(arc.data() + 51, &sz, 4);
     if (len) std::memcpy(arc.data() + 55, in, len);
     const size_t esz = lane_bytes(precision);
-    device_buffer darc, dval;
+    std::lock_guard<std::mutex> chunk_lock(ctx->chunk_mutex);
+    device_buffer& darc = ctx->chunk_a;
+    device_buffer& dval = ctx->chunk_b;
     FB_TRY(darc.ensure(arc.size()));
     FB_TRY(dval.ensure(chunk_n * esz));
     {
@@ -516,6 +531,7 @@ falcon_status falcon_synth_fill_at(int precision, const falcon_synth_spec* s, ui
 
 falcon_status falcon_synth_device(falcon_ctx* ctx, int precision, const falcon_synth_spec* s, uint64_t first,
                                   void* d_out, uint64_t count, void* stream) {
+    FB_NVTX("falcon_synth_device");
     if (!ctx || !s) return set_error(FALCON_ERR_INVALID, "null argument");
     if (s->kind != FALCON_KIND_FIELD)
         return set_error(FALCON_ERR_UNSUPPORTED, "the device generator supports counter-based kinds only");

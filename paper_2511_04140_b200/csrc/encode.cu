@@ -63,6 +63,45 @@ __host__ __device__ __forceinline__ uint32_t encode_stage_bytes(uint32_t chunk_n
     return (uint32_t)(tr::header + (tr::width + 7) / 8 + tr::width * nc + 32 + 15) & ~15u;
 }
 
+// L2 residency of the image ring (FB_L2_HINTS): the streaming value loads are marked
+// evict-first, so the images one wave writes are still in L2 when the next launch places
+// them; after a chunk is placed its image lines are discarded (no write-back of dead data).
+#ifndef FB_L2_HINTS
+#define FB_L2_HINTS 1
+#endif
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
+#if FB_L2_HINTS
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+#else
+    (void)pol;
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ float ld_stream(const float* p, uint64_t pol) {
+#if FB_L2_HINTS
+    float v;
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+#else
+    (void)pol;
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ void l2_discard_line(const void* p) {
+#if FB_L2_HINTS
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+#else
+    (void)p;
+#endif
+}
+
 // 32-bit word of lane values whose byte q is gathered (sb < 4: low word, else high)
 __device__ __forceinline__ uint32_t lane_word(uint64_t z, int sb) { return sb < 4 ? (uint32_t)z : (uint32_t)(z >> 32); }
 __device__ __forceinline__ uint32_t lane_word(uint32_t z, int) { return z; }
@@ -147,15 +186,16 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     T vprev = T(0);
     {
         const T* src = in + v0 + 8u * (uint32_t)tid;
+        const uint64_t pol = l2_evict_first_policy();
         if (len == n && NC == NT) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = __ldg(src + 1 + j);
-            vprev = __ldg(src);
+            for (int j = 0; j < 8; ++j) v[j] = ld_stream(src + 1 + j, pol);
+            vprev = ld_stream(src, pol);
         } else {
             const uint32_t i0 = 8u * (uint32_t)tid;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = (active && i0 + 1 + j < len) ? __ldg(src + 1 + j) : T(0);
-            if (active && i0 < len) vprev = __ldg(src);
+            for (int j = 0; j < 8; ++j) v[j] = (active && i0 + 1 + j < len) ? ld_stream(src + 1 + j, pol) : T(0);
+            if (active && i0 < len) vprev = ld_stream(src, pol);
         }
     }
 
@@ -705,6 +745,20 @@ __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_
             }
         }
     }
+#if FB_L2_HINTS
+    // the warp's 32 images are dead now: drop their L2 lines without a write-back (slots
+    // are whole 128-B lines, encode_slot_bytes); lane L discards lines L, L + 32, ...
+    __syncwarp();
+    for (int q = 0; q < 32; ++q) {
+        const uint64_t cc = t * kPlaceTile + warp * 32 + q;
+        if (cc >= g.n_chunks) break;
+        uint32_t rs = L.place_slot0 + (uint32_t)(cc - L.place_c0);
+        rs = rs >= ws.ring ? rs - (uint32_t)ws.ring : rs;
+        const uint8_t* img = ws.images + rs * (uint64_t)ws.slot;
+        const uint32_t lines = (s_sz[warp * 32 + q] + 4 + 127) >> 7;
+        for (uint32_t ln = lane; ln < lines; ln += 32) l2_discard_line(img + 128 * ln);
+    }
+#endif
 }
 
 // The final placement of a compress call (tiles of the last wave), no encode beside it:
@@ -738,7 +792,8 @@ uint32_t encode_slot_bytes(uint32_t chunk_n) {
     // loads of the placement copy, rounded to 16
     using tr = lane_traits<T>;
     const uint32_t nc = (chunk_n - 1) / 8;
-    return (uint32_t)(tr::header + (tr::width + 7) / 8 + tr::width * nc + 4 + 15) & ~15u;
+    // whole 128-B lines, so a placed image's lines can be discarded (FB_L2_HINTS)
+    return (uint32_t)(tr::header + (tr::width + 7) / 8 + tr::width * nc + 4 + 127) & ~127u;
 }
 
 // Waves: one encode launch covers `wave` batches; its grid row 0 places the tiles the

@@ -55,10 +55,18 @@ template <> struct lane_traits<float> {
 // They are defined (and every device helper below compiled) only in the single
 // kernel translation unit kernels_all.cu, which defines FB200_KERNEL_TU.
 #ifdef FB200_KERNEL_TU
-__device__ double g_pow10_f64[23];
-__device__ float g_pow10_f32[11];
-__device__ uint64_t g_decade_f64[618];  // + guard entry (+inf) for exponent 0x7ff
-__device__ uint32_t g_decade_f32[78];   // + guard entry (+inf) for exponent 0xff
+// In the constant bank (5.4 KB): the encoder's sampling chain (mag_of -> pow10 -> the
+// certification parameters) reads them back to back, and constant-cache hits keep that
+// dependent chain off the L1/L2 path the streaming value loads thrash.
+#ifdef FB_TABLES_GLOBAL
+#define FB_TABLE_SPACE __device__
+#else
+#define FB_TABLE_SPACE __constant__
+#endif
+FB_TABLE_SPACE double g_pow10_f64[23];
+FB_TABLE_SPACE float g_pow10_f32[11];
+FB_TABLE_SPACE uint64_t g_decade_f64[618];  // + guard entry (+inf) for exponent 0x7ff
+FB_TABLE_SPACE uint32_t g_decade_f32[78];   // + guard entry (+inf) for exponent 0xff
 #endif
 
 // Device error word: ((key) << 8) | code, lowest key wins (atomicMin).

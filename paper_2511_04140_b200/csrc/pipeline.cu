@@ -15,6 +15,10 @@
 // put on a host worker; at most n_streams batches in flight (pipeline.hpp:381-452).
 //
 // Host buffers that are already pinned are copied directly (no staging memcpy).
+#include <algorithm>
+#include <functional>
+#include <thread>
+
 #include "runtime.h"
 
 using namespace fb200;
@@ -101,6 +105,7 @@ struct compress_io {
     uint8_t* dst = nullptr;        // buffer mode
     uint64_t dst_cap = 0;
     bool dst_pinned = false;
+    bool frames_only = false;      // one shard of a multi-GPU call: frames at 0, no header
 };
 
 falcon_status run_compress(falcon_ctx* ctx, int prec, compress_io& io,
@@ -124,6 +129,7 @@ falcon_status run_compress(falcon_ctx* ctx, int prec, compress_io& io,
     bool have_batch = false;
     const bool direct_in = io.src && io.src_pinned;
     auto refill = [&]() -> falcon_status {
+        FB_NVTX("compress: source read / staging");
         if (io.src) {
             stage_count = std::min<uint64_t>(bv, io.src_count - src_pos);
             if (direct_in) {
@@ -153,9 +159,10 @@ falcon_status run_compress(falcon_ctx* ctx, int prec, compress_io& io,
     FB_TRY(refill());  // nothing in flight yet: a read error propagates directly
 
     unsigned active = 0, current = 0, next_slot = 0;
-    uint64_t launch_counter = 0, write_cursor = 47, total_values = 0, batch_count = 0;
+    uint64_t launch_counter = 0, write_cursor = io.frames_only ? 0 : 47, total_values = 0, batch_count = 0;
 
     auto launch = [&](pipeline_slot& s, unsigned i) -> falcon_status {
+        FB_NVTX("compress: H2D + encode + size read-back (enqueue)");
         s.count = stage_count;
         s.seq = launch_counter++;
         geometry g;
@@ -221,6 +228,7 @@ falcon_status run_compress(falcon_ctx* ctx, int prec, compress_io& io,
         s.done.reset();
         s.store_started = true;
         pool.submit([&, i] {
+            FB_NVTX("compress: store batch");
             pipeline_slot& sl = *slots[i];
             if (!err.failed.load(std::memory_order_relaxed)) {
                 if (io.store) {  // run_store (pipeline.hpp:237-252)
@@ -314,7 +322,9 @@ falcon_status run_compress(falcon_ctx* ctx, int prec, compress_io& io,
 
     // header last (pipeline.hpp:351-358)
     const archive_header_bytes hdr = header_bytes_of(prec, chunk_n, bv, total_values, batch_count);
-    if (io.store) {
+    if (io.frames_only) {
+        // a shard: the multi-GPU caller writes the one header
+    } else if (io.store) {
         if (io.store(io.suser, 0, hdr.b, 47) != 0)
             return set_error(FALCON_ERR_CALLBACK, "archive store callback failed");
     } else {
@@ -341,11 +351,26 @@ uint32_t rd32(const uint8_t* p) {
     return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
 }
 
+// Batches [b_begin, b_end) whose frames start at `cursor0`; values land at their absolute
+// index (the whole archive: 0, batch_count, 47).  The trailing-bytes check belongs to the
+// range that ends the archive.
+falcon_status run_decompress_range(falcon_ctx* ctx, int prec, const uint8_t* arc, uint64_t len,
+                                   const falcon_archive_info& h, uint64_t b_begin, uint64_t b_end,
+                                   uint64_t cursor0, decompress_io& io, const falcon_pipeline_options& opt,
+                                   falcon_pipeline_stats* stats_out);
+
 falcon_status run_decompress(falcon_ctx* ctx, int prec, const uint8_t* arc, uint64_t len,
                              decompress_io& io, const falcon_pipeline_options& opt,
                              falcon_pipeline_stats* stats_out) {
     falcon_archive_info h;
     FB_TRY(falcon_read_header(arc, len, &h));
+    return run_decompress_range(ctx, prec, arc, len, h, 0, h.batch_count, 47, io, opt, stats_out);
+}
+
+falcon_status run_decompress_range(falcon_ctx* ctx, int prec, const uint8_t* arc, uint64_t len,
+                                   const falcon_archive_info& h, uint64_t b_begin, uint64_t b_end,
+                                   uint64_t cursor0, decompress_io& io, const falcon_pipeline_options& opt,
+                                   falcon_pipeline_stats* stats_out) {
     if (h.precision != prec)
         return set_error(FALCON_ERR_INVALID, "archive precision does not match the requested value type");
     if (opt.n_streams == 0) return set_error(FALCON_ERR_INVALID, "stream count must be positive");
@@ -367,8 +392,8 @@ falcon_status run_decompress(falcon_ctx* ctx, int prec, const uint8_t* arc, uint
         for (auto* s : slots) s->done.wait();
     };
 
-    uint64_t cursor = 47;
-    for (uint64_t b = 0; b < h.batch_count; ++b) {
+    uint64_t cursor = cursor0;
+    for (uint64_t b = b_begin; b < b_end; ++b) {
         if (err.failed.load(std::memory_order_acquire)) break;
         // read_batch (container.cpp:113-132)
         const char* werr = nullptr;
@@ -450,6 +475,7 @@ falcon_status run_decompress(falcon_ctx* ctx, int prec, const uint8_t* arc, uint
         }
         const uint64_t cpb = g.cpb;
         pool.submit([&, i, b, first, count, vals_host, cpb] {
+            FB_NVTX("decompress: wait + put batch");
             pipeline_slot& sl = *slots[i];
             const cudaError_t q = cudaEventSynchronize(sl.ev_data);
             if (q != cudaSuccess) {
@@ -476,12 +502,66 @@ falcon_status run_decompress(falcon_ctx* ctx, int prec, const uint8_t* arc, uint
     }
     drain();
     if (err.failed.load()) return err.raise();
-    if (cursor != len) return set_error(FALCON_ERR_CORRUPT, "trailing bytes after final batch");
+    if (b_end == h.batch_count && cursor != len)
+        return set_error(FALCON_ERR_CORRUPT, "trailing bytes after final batch");
     if (stats_out) {
-        stats_out->batches = h.batch_count;
-        stats_out->values = h.total_values;
+        stats_out->batches = b_end - b_begin;
+        stats_out->values = std::min<uint64_t>(h.total_values, b_end * h.batch_values) -
+                            std::min<uint64_t>(h.total_values, b_begin * h.batch_values);
         stats_out->blocking_waits = 0;
     }
+    return FALCON_OK;
+}
+
+// read_batch over the whole archive on the host (container.cpp:113-132): frame offsets
+// off[0..B], off[B] = end of the last frame; the reference's messages and batch suffix.
+falcon_status walk_frames_host(const uint8_t* arc, uint64_t len, const falcon_archive_info& h,
+                               std::vector<uint64_t>& off) {
+    off.assign(h.batch_count + 1, 0);
+    uint64_t cursor = 47;
+    const uint64_t n = h.chunk_n;
+    for (uint64_t b = 0; b < h.batch_count; ++b) {
+        off[b] = cursor;
+        const char* werr = nullptr;
+        const uint64_t rem = len - cursor;
+        uint64_t cnt = 0, table = 0, payload = 0;
+        if (rem < 4) {
+            werr = "batch header truncated";
+        } else {
+            cnt = rd32(arc + cursor);
+            table = 4 + 4 * cnt;
+            if (rem < table) {
+                werr = "batch size table truncated";
+            } else {
+                for (uint64_t i = 0; i < cnt; ++i) payload += rd32(arc + cursor + 4 + 4 * i);
+                if (rem - table < payload) werr = "batch payload truncated";
+            }
+        }
+        const uint64_t count = std::min<uint64_t>(h.batch_values, h.total_values - b * h.batch_values);
+        if (!werr && cnt != (count + n - 1) / n) werr = "chunk count mismatch";
+        if (werr) return set_error(FALCON_ERR_CORRUPT, std::string(werr) + " (batch " + std::to_string(b) + ")");
+        cursor += table + payload;
+    }
+    off[h.batch_count] = cursor;
+    if (cursor != len) return set_error(FALCON_ERR_CORRUPT, "trailing bytes after final batch");
+    return FALCON_OK;
+}
+
+// Runs fn(g) for every context on its own host thread; the error of the lowest-numbered
+// failing context is returned (its message re-raised on the calling thread).
+falcon_status run_on_contexts(unsigned n, const std::function<falcon_status(unsigned)>& fn) {
+    std::vector<falcon_status> st(n, FALCON_OK);
+    std::vector<std::string> msg(n);
+    std::vector<std::thread> th;
+    th.reserve(n);
+    for (unsigned g = 0; g < n; ++g)
+        th.emplace_back([&, g] {
+            st[g] = fn(g);
+            if (st[g] != FALCON_OK) msg[g] = falcon_last_error();
+        });
+    for (auto& t : th) t.join();
+    for (unsigned g = 0; g < n; ++g)
+        if (st[g] != FALCON_OK) return set_error(st[g], msg[g]);
     return FALCON_OK;
 }
 
@@ -499,6 +579,7 @@ falcon_status falcon_compress_stream(falcon_ctx* ctx, int precision, falcon_read
                                      void* read_user, falcon_store_fn store, void* store_user,
                                      const falcon_pipeline_options* opt,
                                      falcon_pipeline_stats* stats) {
+    FB_NVTX("falcon_compress_stream");
     if (!ctx || !read || !store) return set_error(FALCON_ERR_INVALID, "null argument");
     std::lock_guard<std::mutex> lock(ctx->api_mutex);
     device_guard dg(ctx->device);
@@ -515,6 +596,7 @@ falcon_status falcon_compress_host(falcon_ctx* ctx, int precision, const void* v
                                    uint64_t n_values, const falcon_pipeline_options* opt,
                                    uint8_t* out, uint64_t out_cap, uint64_t* out_bytes,
                                    falcon_pipeline_stats* stats) {
+    FB_NVTX("falcon_compress_host");
     if (!ctx || (!values && n_values) || !out) return set_error(FALCON_ERR_INVALID, "null argument");
     std::lock_guard<std::mutex> lock(ctx->api_mutex);
     device_guard dg(ctx->device);
@@ -531,10 +613,110 @@ falcon_status falcon_compress_host(falcon_ctx* ctx, int precision, const void* v
     return FALCON_OK;
 }
 
+falcon_status falcon_compress_host_multi(falcon_ctx* const* ctxs, unsigned n_ctx, int precision,
+                                         const void* values, uint64_t n_values,
+                                         const falcon_pipeline_options* opt, uint8_t* out, uint64_t out_cap,
+                                         uint64_t* out_bytes, falcon_pipeline_stats* stats) {
+    FB_NVTX("falcon_compress_host_multi");
+    if (!ctxs || n_ctx == 0 || (!values && n_values) || !out) return set_error(FALCON_ERR_INVALID, "null argument");
+    for (unsigned g = 0; g < n_ctx; ++g)
+        if (!ctxs[g]) return set_error(FALCON_ERR_INVALID, "null context");
+    const falcon_pipeline_options o = resolve(opt);
+    FB_TRY(validate_options(o.chunk_n, o.batch_values));
+    const size_t esz = lane_bytes(precision);
+    const uint64_t bv = o.batch_values;
+    const uint64_t B = (n_values + bv - 1) / bv;
+    // batch-range shards: context g owns batches [gB/G, (g+1)B/G)
+    std::vector<uint64_t> b0(n_ctx + 1);
+    for (unsigned g = 0; g <= n_ctx; ++g) b0[g] = B * g / n_ctx;
+    std::vector<std::vector<uint8_t>> frames(n_ctx);
+    std::vector<falcon_pipeline_stats> st(n_ctx);
+    std::vector<uint64_t> bytes(n_ctx, 0);
+    FB_TRY(run_on_contexts(n_ctx, [&](unsigned g) -> falcon_status {
+        const uint64_t v0 = std::min(n_values, b0[g] * bv), v1 = std::min(n_values, b0[g + 1] * bv);
+        if (v1 == v0) return FALCON_OK;
+        falcon_ctx* ctx = ctxs[g];
+        std::lock_guard<std::mutex> lock(ctx->api_mutex);
+        device_guard dg(ctx->device);
+        frames[g].resize(falcon_compress_bound(precision, v1 - v0, o.chunk_n, bv));
+        compress_io io;
+        io.src = static_cast<const uint8_t*>(values) + v0 * esz;
+        io.src_count = v1 - v0;
+        io.src_pinned = is_pinned(values);
+        io.dst = frames[g].data();
+        io.dst_cap = frames[g].size();
+        io.frames_only = true;
+        FB_TRY(run_compress(ctx, precision, io, o, &st[g]));
+        bytes[g] = ctx->last_archive_bytes;
+        return FALCON_OK;
+    }));
+    uint64_t total = 47;
+    for (unsigned g = 0; g < n_ctx; ++g) total += bytes[g];
+    if (total > out_cap) return set_error(FALCON_ERR_CAPACITY, "output capacity too small for the compressed archive");
+    const archive_header_bytes hdr = header_bytes_of(precision, o.chunk_n, bv, n_values, B);
+    std::memcpy(out, hdr.b, 47);
+    uint64_t at = 47;
+    for (unsigned g = 0; g < n_ctx; ++g) {
+        if (bytes[g]) std::memcpy(out + at, frames[g].data(), bytes[g]);
+        at += bytes[g];
+    }
+    if (out_bytes) *out_bytes = total;
+    if (stats) {
+        *stats = falcon_pipeline_stats{};
+        for (auto& x : st) {
+            stats->batches += x.batches;
+            stats->values += x.values;
+            stats->blocking_waits += x.blocking_waits;
+        }
+    }
+    return FALCON_OK;
+}
+
+falcon_status falcon_decompress_host_multi(falcon_ctx* const* ctxs, unsigned n_ctx, int precision,
+                                           const uint8_t* archive, uint64_t archive_bytes, void* values,
+                                           uint64_t cap_values, uint64_t* n_values,
+                                           const falcon_pipeline_options* opt, falcon_pipeline_stats* stats) {
+    FB_NVTX("falcon_decompress_host_multi");
+    if (!ctxs || n_ctx == 0 || (!archive && archive_bytes)) return set_error(FALCON_ERR_INVALID, "null argument");
+    for (unsigned g = 0; g < n_ctx; ++g)
+        if (!ctxs[g]) return set_error(FALCON_ERR_INVALID, "null context");
+    falcon_archive_info h;
+    FB_TRY(falcon_read_header(archive, archive_bytes, &h));
+    if (h.precision != precision)
+        return set_error(FALCON_ERR_INVALID, "archive precision does not match the requested value type");
+    if (h.total_values > cap_values) return set_error(FALCON_ERR_CAPACITY, "value capacity too small for the archive");
+    const falcon_pipeline_options o = resolve(opt);
+    // the one sequential step: locate every frame (size tables only), then shard by batch
+    std::vector<uint64_t> off;
+    FB_TRY(walk_frames_host(archive, archive_bytes, h, off));
+    const uint64_t B = h.batch_count;
+    std::vector<falcon_pipeline_stats> st(n_ctx);
+    FB_TRY(run_on_contexts(n_ctx, [&](unsigned g) -> falcon_status {
+        const uint64_t lo = B * g / n_ctx, hi = B * (g + 1) / n_ctx;
+        if (lo == hi) return FALCON_OK;
+        falcon_ctx* ctx = ctxs[g];
+        std::lock_guard<std::mutex> lock(ctx->api_mutex);
+        device_guard dg(ctx->device);
+        decompress_io io;
+        io.dst = static_cast<uint8_t*>(values);
+        io.dst_cap = cap_values;
+        io.dst_pinned = is_pinned(values);
+        return run_decompress_range(ctx, precision, archive, archive_bytes, h, lo, hi, off[lo], io, o, &st[g]);
+    }));
+    if (n_values) *n_values = h.total_values;
+    if (stats) {
+        *stats = falcon_pipeline_stats{};
+        stats->batches = h.batch_count;
+        stats->values = h.total_values;
+    }
+    return FALCON_OK;
+}
+
 falcon_status falcon_decompress_stream(falcon_ctx* ctx, int precision, const uint8_t* archive,
                                        uint64_t archive_bytes, falcon_put_fn put, void* put_user,
                                        const falcon_pipeline_options* opt,
                                        falcon_pipeline_stats* stats) {
+    FB_NVTX("falcon_decompress_stream");
     if (!ctx || !put || (!archive && archive_bytes)) return set_error(FALCON_ERR_INVALID, "null argument");
     std::lock_guard<std::mutex> lock(ctx->api_mutex);
     device_guard dg(ctx->device);
@@ -549,6 +731,7 @@ falcon_status falcon_decompress_host(falcon_ctx* ctx, int precision, const uint8
                                      uint64_t archive_bytes, void* values, uint64_t cap_values,
                                      uint64_t* n_values, const falcon_pipeline_options* opt,
                                      falcon_pipeline_stats* stats) {
+    FB_NVTX("falcon_decompress_host");
     if (!ctx || (!archive && archive_bytes)) return set_error(FALCON_ERR_INVALID, "null argument");
     std::lock_guard<std::mutex> lock(ctx->api_mutex);
     device_guard dg(ctx->device);

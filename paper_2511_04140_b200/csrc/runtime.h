@@ -16,6 +16,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/falcon_b200.h"
 #include "kernels.h"
@@ -40,6 +41,16 @@ falcon_status device_error_status(uint32_t code);
         falcon_status fb_s_ = (x);                                                          \
         if (fb_s_ != FALCON_OK) return fb_s_;                                               \
     } while (0)
+
+// ---- NVTX: every C-ABI entry point and every host pipeline stage is a named range, so
+//      an nsys / ncu timeline shows API calls, per-batch H2D / encode / D2H / store ----
+struct nvtx_scope {
+    explicit nvtx_scope(const char* name) { nvtxRangePushA(name); }
+    ~nvtx_scope() { nvtxRangePop(); }
+    nvtx_scope(const nvtx_scope&) = delete;
+    nvtx_scope& operator=(const nvtx_scope&) = delete;
+};
+#define FB_NVTX(name) ::fb200::nvtx_scope fb_nvtx_scope_(name)
 
 // ---- format helpers (host) ----------------------------------------------------
 inline size_t lane_bytes(int prec) { return prec == FALCON_F64 ? 8 : 4; }
@@ -157,6 +168,8 @@ struct falcon_ctx {
     // device-resident API scratch
     fb200::device_buffer enc_status, dec_off, dec_size, dec_ready, misc;
     fb200::pinned_buffer host_box;  // pinned mailbox for the sync device APIs
+    fb200::device_buffer chunk_a, chunk_b;   // per-chunk operator scratch (chunk_workspace)
+    std::mutex chunk_mutex;
     // host pipeline
     std::vector<std::unique_ptr<fb200::pipeline_slot>> slots;
     fb200::pinned_buffer stage;     // extra input staging buffer swapped into slots

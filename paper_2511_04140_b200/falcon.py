@@ -30,7 +30,7 @@ EXPORTED = [
     "falcon_ctx_sync", "falcon_compress_stream", "falcon_decompress_stream", "falcon_compress_host",
     "falcon_decompress_host", "falcon_compress_chunk", "falcon_decompress_chunk", "falcon_synth_fill",
     "falcon_ctx_set_kernel_events", "falcon_selftest_dp", "falcon_selftest_div",
-    "falcon_synth_fill_at", "falcon_synth_device",
+    "falcon_synth_fill_at", "falcon_synth_device", "falcon_compress_host_multi", "falcon_decompress_host_multi",
 ]
 
 
@@ -124,6 +124,10 @@ def load() -> C.CDLL:
     L.falcon_compress_chunk.argtypes = [vp, i32, vp, u32, vp, u64, C.POINTER(u64)]
     L.falcon_decompress_chunk.argtypes = [vp, i32, vp, u64, u32, u32, vp]
     L.falcon_synth_fill.argtypes = [i32, C.POINTER(SynthSpec), vp, u64]
+    L.falcon_compress_host_multi.argtypes = [C.POINTER(vp), u32, i32, vp, u64, C.POINTER(PipelineOptions), vp, u64,
+                                             C.POINTER(u64), C.POINTER(PipelineStats)]
+    L.falcon_decompress_host_multi.argtypes = [C.POINTER(vp), u32, i32, vp, u64, vp, u64, C.POINTER(u64),
+                                               C.POINTER(PipelineOptions), C.POINTER(PipelineStats)]
     L.falcon_synth_fill_at.argtypes = [i32, C.POINTER(SynthSpec), u64, vp, u64]
     L.falcon_synth_device.argtypes = [vp, i32, C.POINTER(SynthSpec), u64, vp, u64, vp]
     L.falcon_default_options.argtypes = [C.POINTER(PipelineOptions)]
@@ -188,6 +192,34 @@ def synth(kind: str, count: int, prec: int = F64, dp: int = 2, seed: int = 1, st
         out = np.empty(count, np.float64 if prec == F64 else np.float32)
     _check(load().falcon_synth_fill_at(prec, C.byref(s), first, _np_ptr(out), count))
     return out
+
+
+def compress_host_multi(codecs, values: np.ndarray, opt: PipelineOptions | None = None,
+                        stats: PipelineStats | None = None) -> np.ndarray:
+    """Host-resident compress across several GPUs (one Codec per GPU), batch-range shards
+    (falcon_compress_host_multi): bytes equal a single-GPU compress_host."""
+    prec = prec_of(values.dtype)
+    opt = opt or options()
+    v = np.ascontiguousarray(values)
+    out = np.empty(compress_bound(prec, len(v), opt.chunk_n, opt.batch_values), np.uint8)
+    arr = (C.c_void_p * len(codecs))(*[c.ctx.value for c in codecs])
+    nb = C.c_uint64()
+    _check(load().falcon_compress_host_multi(arr, len(codecs), prec, _np_ptr(v), len(v), C.byref(opt), _np_ptr(out),
+                                             len(out), C.byref(nb), C.byref(stats) if stats else None))
+    return out[: nb.value]
+
+
+def decompress_host_multi(codecs, archive, prec: int = F64, opt: PipelineOptions | None = None,
+                          out: np.ndarray | None = None) -> np.ndarray:
+    a = np.frombuffer(archive, np.uint8) if isinstance(archive, (bytes, bytearray)) else archive
+    total = int.from_bytes(bytes(a[23:31]), "little") if len(a) >= 47 else 0
+    if out is None:
+        out = np.empty(max(total, 1), np.float64 if prec == F64 else np.float32)
+    arr = (C.c_void_p * len(codecs))(*[c.ctx.value for c in codecs])
+    nv = C.c_uint64()
+    _check(load().falcon_decompress_host_multi(arr, len(codecs), prec, _np_ptr(a), len(a), _np_ptr(out), len(out),
+                                               C.byref(nv), C.byref(opt or options()), None))
+    return out[: nv.value]
 
 
 class Codec:

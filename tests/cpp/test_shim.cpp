@@ -271,6 +271,18 @@ int main() {
         auto bad = golden;
         bad[11] |= 0x40;
         CHECK_THROWS_WITH(fb::decompress_chunk<double>(bad, 65, 65), fb::corrupt_error, "nonzero flag padding bits");
+        // workspace forms (chunk_codec.hpp:50-131): compress appends, decompress resizes,
+        // one workspace reused across chunks of both kinds
+        fb::chunk_workspace<double> ws;
+        std::vector<std::uint8_t> stream{0xAB};
+        fb::compress_chunk<double>(std::span<const double>(sp), ws, stream);
+        fb::compress_chunk<double>(std::span<const double>(z), ws, stream);
+        CHECK(stream.size() == 1 + golden.size() + 11 && stream[0] == 0xAB);
+        CHECK(std::equal(golden.begin(), golden.end(), stream.begin() + 1));
+        std::vector<double> back(7, -1.0);
+        fb::decompress_chunk<double>(std::span<const std::uint8_t>(stream.data() + 1, golden.size()), 65, 40, ws,
+                                     back);
+        CHECK(back.size() == 40 && same_bits(back, std::vector<double>(sp.begin(), sp.begin() + 40)));
     }
     std::printf("%d checks, %d failures\n", g_checks, g_failures);
     return g_failures ? 1 : 0;

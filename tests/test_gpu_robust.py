@@ -110,3 +110,39 @@ def test_capacity_overflow_on_the_chained_path(codec, oracle):
     arc, nb = codec.compress_device(d, 1025, 1025 * 16)
     assert arc[:nb].cpu().numpy().tobytes() == want
     assert bits(codec.decompress_device(arc, nb).cpu().numpy()) == bits(vals)
+
+
+@pytest.mark.parametrize("kind,prec", [("walk", F64), ("outlier", F64), ("mixed", 1)])
+def test_random_corruption_fuzz_matches_oracle(codec, oracle, kind, prec):
+    # mutations of a multi-batch archive (byte flips anywhere after the header, truncations,
+    # inserted bytes): the device decoder either fails with the oracle's exact error text
+    # or returns the oracle's exact values (test_oracle_vs_ref.py:36 does this CPU-side)
+    vals = synth(kind, 5 * 1025 * 3 + 211, prec, seed=21, period=100)
+    arc = oracle.compress_archive(vals, 1025, 1025 * 3)
+    rng = np.random.default_rng(77 + prec)
+    for trial in range(150):
+        a = bytearray(arc)
+        r = trial % 5
+        if r == 0:
+            a = a[: int(rng.integers(47, len(a)))]
+        elif r == 1:
+            pos = int(rng.integers(47, len(a)))
+            a[pos:pos] = bytes([int(rng.integers(0, 256))])
+        else:
+            for _ in range(1 + r // 3):
+                pos = int(rng.integers(47, len(a)))
+                a[pos] ^= int(rng.integers(1, 256))
+        a = bytes(a)
+        try:
+            want_vals = oracle.decompress_archive(a, prec)
+            want_msg = None
+        except Exception as e:  # noqa: BLE001
+            want_vals, want_msg = None, e.message
+        t = torch.frombuffer(bytearray(a), dtype=torch.uint8).cuda()
+        if want_msg is None:
+            got = codec.decompress_device(t, len(a)).cpu().numpy()
+            assert bits(got) == bits(want_vals), f"trial {trial}: values differ"
+        else:
+            with pytest.raises(FalconError) as ei:
+                codec.decompress_device(t, len(a))
+            assert str(ei.value) == want_msg, f"trial {trial}"
