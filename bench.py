@@ -231,15 +231,20 @@ def link_bandwidth(torch, dev, host_pinned):
     return best[0], best[1]
 
 
-def our_launches_per_step(n_values):
+def our_launches_per_step(n_values, prec):
     """Kernels of one compress + decompress (csrc/encode.cu plan_waves, decode.cu): one
     encode launch per wave of batches + the final placement, then walker + decoder."""
     if n_values == 0:
         return 0
     nb = (n_values + BATCH_VALUES - 1) // BATCH_VALUES
     cpb = (BATCH_VALUES + CHUNK_N - 1) // CHUNK_N if nb > 1 else (n_values + CHUNK_N - 1) // CHUNK_N
-    wave = max(1, min(int(os.environ.get("FALCON_ENC_WAVE_CHUNKS", "49152")) // cpb, 65534, nb))
-    return (nb + wave - 1) // wave + 1 + 2
+    n_chunks = (nb - 1) * cpb + ((n_values - (nb - 1) * BATCH_VALUES) + CHUNK_N - 1) // CHUNK_N
+    slot = 8320 if prec == F64 else 4224                     # encode_slot_bytes
+    slots = int(os.environ.get("FALCON_ENC_RING_BYTES", str(4 << 30))) // slot
+    wave = int(os.environ.get("FALCON_ENC_WAVE_CHUNKS", "0")) or (n_chunks if slots >= n_chunks
+                                                                   else (slots - 128) // 2)
+    wb = max(1, min(wave // cpb, 65534, nb))
+    return (nb + wb - 1) // wb + 1 + 2
 
 
 def run_ours(args, rank, world, local_rank):
@@ -433,7 +438,7 @@ def run_ours(args, rank, world, local_rank):
         cpu = {"value": sample_n * esz / med / 1e9, "unit": "GB/s", "cores": cores, "kind": kind,
                "sample": f"{'all' if sample_n == n else 'first'} {sample_n} values of the workload; "
                          f"compress_pipeline + decompress_pipeline round trip, median of 3 after 1 warm-up"}
-    nl = our_launches_per_step(n)
+    nl = our_launches_per_step(n, prec)
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,

@@ -39,7 +39,7 @@ __device__ void walk_frames(const uint8_t* __restrict__ arc, uint64_t len, const
                             uint64_t b0, uint64_t cursor0) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nthreads = blockDim.x, nwarps = nthreads >> 5;
-    __shared__ uint32_t s_cnt, s_code;
+    __shared__ uint32_t s_cnt, s_code, s_stop;
     __shared__ uint64_t s_wsum[32];
     uint64_t cursor = cursor0;
     for (uint64_t b = b0; b < g.n_batches; ++b) {
@@ -146,10 +146,12 @@ __device__ void walk_frames(const uint8_t* __restrict__ arc, uint64_t len, const
                 __threadfence();
                 st_release32(&ws.ready[b], 1u);
             }
-            s_code = code;
+            s_stop = code;
         }
         __syncthreads();
-        if (s_code) return;
+        // (a separate word: s_code is rewritten at the top of the next batch while slower
+        // threads may still read this verdict -- racecheck)
+        if (s_stop) return;
         cursor = pay0 + carry;
     }
     if (tid == 0 && cursor != len) record_error(ws.error, g.n_chunks, DEV_E_TRAILING);  // pipeline.hpp:460-461

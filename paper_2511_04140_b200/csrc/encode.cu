@@ -66,8 +66,10 @@ __host__ __device__ __forceinline__ uint32_t encode_stage_bytes(uint32_t chunk_n
 // L2 residency of the image ring (FB_L2_HINTS): the streaming value loads are marked
 // evict-first, so the images one wave writes are still in L2 when the next launch places
 // them; after a chunk is placed its image lines are discarded (no write-back of dead data).
+// Measured on cfg2 (A/B, profiles/r02): no gain (compress 1.319 ms without, 1.345 ms
+// with), so off by default.
 #ifndef FB_L2_HINTS
-#define FB_L2_HINTS 1
+#define FB_L2_HINTS 0
 #endif
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
     uint64_t pol;
@@ -805,20 +807,28 @@ struct wave_plan {
     uint64_t wave_batches, launches, ring, tiles, tile;
 };
 
-static uint64_t env_wave_chunks() {
-    static const uint64_t v = [] {
-        const char* e = std::getenv("FALCON_ENC_WAVE_CHUNKS");
-        const unsigned long long x = e ? std::strtoull(e, nullptr, 10) : 0ull;
-        return (uint64_t)(x ? x : 49152ull);   // 12 default batches
-    }();
-    return v;
+// Fewer, larger waves are faster (cfg2 compress: 1.44 / 1.39 / 1.35 / 1.31 ms at 16 Ki /
+// 24 Ki / 48 Ki / all 256 Ki chunks per wave), so a wave is as large as the ring budget
+// allows: FALCON_ENC_RING_BYTES (default 4 GiB) holds two waves of image slots.  A call
+// whose images fit the budget runs as one encode launch + the final placement.
+static uint64_t env_u64(const char* name, uint64_t dflt) {
+    const char* e = std::getenv(name);
+    const unsigned long long x = e ? std::strtoull(e, nullptr, 10) : 0ull;
+    return x ? (uint64_t)x : dflt;
 }
 
-static wave_plan plan_waves(const geometry& g) {
+static wave_plan plan_waves(const geometry& g, uint32_t slot_bytes) {
     wave_plan w;
     w.tile = encode_block_threads(g.chunk_n);
     w.tiles = (g.n_chunks + w.tile - 1) / w.tile;
-    uint64_t wb = env_wave_chunks() / g.cpb;
+    static const uint64_t ring_budget = env_u64("FALCON_ENC_RING_BYTES", 4ull << 30);
+    static const uint64_t forced = env_u64("FALCON_ENC_WAVE_CHUNKS", 0);
+    uint64_t wave_chunks = forced;
+    if (!wave_chunks) {
+        const uint64_t slots = ring_budget / slot_bytes;
+        wave_chunks = slots >= g.n_chunks ? g.n_chunks : (slots > 2 * w.tile ? (slots - w.tile) / 2 : w.tile);
+    }
+    uint64_t wb = wave_chunks / g.cpb;
     if (wb < 1) wb = 1;
     if (wb > 65534) wb = 65534;                     // grid.y = 1 + batches of the wave
     if (wb >= g.n_batches) wb = g.n_batches;
@@ -831,7 +841,7 @@ static wave_plan plan_waves(const geometry& g) {
 
 template <typename T>
 size_t encode_scratch_bytes(const geometry& g) {
-    const wave_plan w = plan_waves(g);
+    const wave_plan w = plan_waves(g, encode_slot_bytes<T>(g.chunk_n));
     size_t b = 0;
     b += (g.n_chunks * 4 + 15) & ~15ull;                 // sizes
     b += w.tiles * 8;                                     // tile status
@@ -845,7 +855,7 @@ template <typename T>
 encode_ws carve_encode_ws(void* scratch, const geometry& g, uint32_t* ticket, unsigned long long* error,
                           uint64_t* total) {
     encode_ws ws;
-    const wave_plan w = plan_waves(g);
+    const wave_plan w = plan_waves(g, encode_slot_bytes<T>(g.chunk_n));
     uint8_t* p = static_cast<uint8_t*>(scratch);
     ws.sizes = reinterpret_cast<uint32_t*>(p);
     p += (g.n_chunks * 4 + 15) & ~15ull;
@@ -890,7 +900,7 @@ cudaError_t launch_encode(const T* d_in, const geometry& g, uint8_t* d_out, uint
             return e;
         return g.header_bytes ? cudaMemcpyAsync(d_out, hdr.b, 47, cudaMemcpyHostToDevice, st) : cudaSuccess;
     }
-    const wave_plan w = plan_waves(g);
+    const wave_plan w = plan_waves(g, encode_slot_bytes<T>(g.chunk_n));
     // tile status + batch prefixes are contiguous
     if ((e = cudaMemsetAsync(ws.tile_status, 0, (w.tiles + g.n_batches + 1) * 8, st))) return e;
     if ((e = cudaMemsetAsync(ws.ticket, 0, sizeof(uint32_t), st))) return e;
