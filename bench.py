@@ -243,7 +243,7 @@ def our_launches_per_step(n_values, prec):
     slots = int(os.environ.get("FALCON_ENC_RING_BYTES", str(4 << 30))) // slot
     wave = int(os.environ.get("FALCON_ENC_WAVE_CHUNKS", "0")) or (n_chunks if slots >= n_chunks
                                                                    else (slots - 128) // 2)
-    wb = max(1, min(wave // cpb, 65534, nb))
+    wb = nb if wave >= n_chunks else max(1, min(wave // cpb, 65534, nb))
     return (nb + wb - 1) // wb + 1 + 2
 
 

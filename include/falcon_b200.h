@@ -128,6 +128,13 @@ falcon_status falcon_compress_device_async(falcon_ctx* ctx, int precision, const
                                            uint64_t n_values, uint32_t chunk_n,
                                            uint64_t batch_values, void* d_out, uint64_t out_cap,
                                            uint64_t* d_out_bytes, void* stream);
+/* Frames only: the batch frames of n_values values with no 47-byte header -- one shard of
+ * a larger archive (frames are context-free, container.cpp:88-111).  Asynchronous like
+ * falcon_compress_device_async; the byte total goes to d_out_bytes (device u64). */
+falcon_status falcon_compress_device_frames(falcon_ctx* ctx, int precision, const void* d_values,
+                                            uint64_t n_values, uint32_t chunk_n,
+                                            uint64_t batch_values, void* d_out, uint64_t out_cap,
+                                            uint64_t* d_out_bytes, void* stream);
 /* Decompress the archive at d_archive (archive_bytes long) into d_values (cap_values).
  * Reads the header back to the host first; synchronises `stream`. */
 falcon_status falcon_decompress_device(falcon_ctx* ctx, int precision, const void* d_archive,
@@ -210,6 +217,20 @@ falcon_status falcon_decompress_host_multi(falcon_ctx* const* ctxs, unsigned n_c
                                            void* values, uint64_t cap_values, uint64_t* n_values,
                                            const falcon_pipeline_options* opt,
                                            falcon_pipeline_stats* stats);
+
+/* ---- files through GPU-direct storage ----
+ * Raw value files are read straight into device memory with cuFile (GPUDirect Storage,
+ * or cuFile's compat path) when libcufile is present, else through a pinned bounce
+ * buffer; *io_path (optional) gets 1 for cuFile, 0 for the bounce path.  Compress runs the
+ * device codec over windows of whole batches and writes frames, then the header: the
+ * archive equals falcon_compress_host's.  Decompress reads the archive into HBM, indexes
+ * its frames on the device and decodes batch windows into the raw file. */
+falcon_status falcon_compress_file(falcon_ctx* ctx, int precision, const char* raw_path,
+                                   const char* archive_path, const falcon_pipeline_options* opt,
+                                   uint64_t* archive_bytes, int* io_path);
+falcon_status falcon_decompress_file(falcon_ctx* ctx, int precision, const char* archive_path,
+                                     const char* raw_path, const falcon_pipeline_options* opt,
+                                     uint64_t* n_values, int* io_path);
 
 /* ---- per-chunk operators (GPU-backed; host buffers) ---- */
 /* Encodes exactly chunk_n values; returns the encoded length in *out_len. */

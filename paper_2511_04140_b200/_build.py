@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # CPU reference bit for bit (the kernels also use explicit __dmul_rn/__ddiv_rn).
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
          "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I", os.path.join(ROOT, "include")]
-UNITS = ["kernels_all.cu", "capi.cu", "runtime.cu", "pipeline.cu"]
+UNITS = ["kernels_all.cu", "capi.cu", "runtime.cu", "pipeline.cu", "gds.cu"]
 HEADERS = ["falcon_common.cuh", "kernels.h", "runtime.h", "encode.cu", "decode.cu", "tables.cu", "selftest.cu",
            "synth.cu", "field.cuh", "dpds.cuh", "launch_cache.cuh"]
 

@@ -60,13 +60,13 @@ decode_ws ctx_decode_ws(falcon_ctx* ctx) {
 
 falcon_status enqueue_compress(falcon_ctx* ctx, int prec, const void* d_values, uint64_t n,
                                uint32_t chunk_n, uint64_t bv, void* d_out, uint64_t cap,
-                               uint64_t* d_total, cudaStream_t st, geometry& g) {
+                               uint64_t* d_total, cudaStream_t st, geometry& g, uint64_t header_bytes = 47) {
     FB_TRY(validate_options(chunk_n, bv));
-    FB_TRY(make_geometry(n, chunk_n, bv, 47, g));
+    FB_TRY(make_geometry(n, chunk_n, bv, header_bytes, g));
     const size_t scratch = prec == FALCON_F64 ? encode_scratch_bytes<double>(g) : encode_scratch_bytes<float>(g);
     FB_TRY(ctx->enc_status.ensure(scratch));
     const archive_header_bytes hdr = header_bytes_of(prec, chunk_n, bv, n, g.n_batches);
-    if (cap < 47) return set_error(FALCON_ERR_CAPACITY, "output capacity too small for the header");
+    if (cap < header_bytes) return set_error(FALCON_ERR_CAPACITY, "output capacity too small for the header");
     uint32_t* ticket = reinterpret_cast<uint32_t*>(misc_at(ctx, kEncTicket));
     auto* err = reinterpret_cast<unsigned long long*>(misc_at(ctx, kEncError));
     uint64_t* total = d_total ? d_total : reinterpret_cast<uint64_t*>(misc_at(ctx, kEncTotal));
@@ -229,6 +229,18 @@ falcon_status falcon_compress_device_async(falcon_ctx* ctx, int precision, const
     geometry g;
     return enqueue_compress(ctx, precision, d_values, n_values, chunk_n, batch_values, d_out, out_cap,
                             d_out_bytes, static_cast<cudaStream_t>(stream), g);
+}
+
+falcon_status falcon_compress_device_frames(falcon_ctx* ctx, int precision, const void* d_values,
+                                            uint64_t n_values, uint32_t chunk_n, uint64_t batch_values,
+                                            void* d_out, uint64_t out_cap, uint64_t* d_out_bytes, void* stream) {
+    FB_NVTX("falcon_compress_device_frames");
+    if (!ctx || !d_out_bytes) return set_error(FALCON_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lock(ctx->api_mutex);
+    device_guard dg(ctx->device);
+    geometry g;
+    return enqueue_compress(ctx, precision, d_values, n_values, chunk_n, batch_values, d_out, out_cap,
+                            d_out_bytes, static_cast<cudaStream_t>(stream), g, 0);
 }
 
 falcon_status falcon_compress_device(falcon_ctx* ctx, int precision, const void* d_values,

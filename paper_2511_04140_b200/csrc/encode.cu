@@ -828,7 +828,7 @@ static wave_plan plan_waves(const geometry& g, uint32_t slot_bytes) {
         const uint64_t slots = ring_budget / slot_bytes;
         wave_chunks = slots >= g.n_chunks ? g.n_chunks : (slots > 2 * w.tile ? (slots - w.tile) / 2 : w.tile);
     }
-    uint64_t wb = wave_chunks / g.cpb;
+    uint64_t wb = wave_chunks >= g.n_chunks ? g.n_batches : wave_chunks / g.cpb;
     if (wb < 1) wb = 1;
     if (wb > 65534) wb = 65534;                     // grid.y = 1 + batches of the wave
     if (wb >= g.n_batches) wb = g.n_batches;

@@ -1,0 +1,286 @@
+// gds.cu -- file <-> device paths for the host-resident configs:
+// raw value files are read straight into HBM through cuFile (GPUDirect Storage, or
+// cuFile's own compat path where the nvidia-fs driver is absent), compressed by the
+// device-resident codec in windows of whole batches, and the frames written out; the
+// inverse reads the archive into HBM, indexes its frames on the device and decodes batch
+// windows into the raw file.  libcufile is loaded with dlopen: without it (or on a file
+// system cuFile cannot register) reads go through a pinned bounce buffer instead.
+#include <cufile.h>
+#include <dlfcn.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cerrno>
+
+#include "runtime.h"
+
+using namespace fb200;
+
+namespace {
+
+struct cufile_api {
+    bool ok = false;
+    CUfileError_t (*driver_open)() = nullptr;
+    CUfileError_t (*handle_register)(CUfileHandle_t*, CUfileDescr_t*) = nullptr;
+    void (*handle_deregister)(CUfileHandle_t) = nullptr;
+    ssize_t (*read)(CUfileHandle_t, void*, size_t, off_t, off_t) = nullptr;
+};
+
+const cufile_api& cufile() {
+    static const cufile_api api = [] {
+        cufile_api a;
+        if (std::getenv("FALCON_NO_CUFILE")) return a;
+        void* h = dlopen("libcufile.so.0", RTLD_NOW | RTLD_LOCAL);
+        if (!h) h = dlopen("libcufile.so", RTLD_NOW | RTLD_LOCAL);
+        if (!h) return a;
+        a.driver_open = reinterpret_cast<decltype(a.driver_open)>(dlsym(h, "cuFileDriverOpen"));
+        a.handle_register = reinterpret_cast<decltype(a.handle_register)>(dlsym(h, "cuFileHandleRegister"));
+        a.handle_deregister = reinterpret_cast<decltype(a.handle_deregister)>(dlsym(h, "cuFileHandleDeregister"));
+        a.read = reinterpret_cast<decltype(a.read)>(dlsym(h, "cuFileRead"));
+        if (!a.driver_open || !a.handle_register || !a.handle_deregister || !a.read) return a;
+        a.ok = a.driver_open().err == CU_FILE_SUCCESS;
+        return a;
+    }();
+    return api;
+}
+
+struct device_guard {
+    int prev = -1;
+    explicit device_guard(int d) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != d) cudaSetDevice(d);
+    }
+    ~device_guard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// A file opened for device reads: a cuFile handle when one registers (O_DIRECT first,
+// then a buffered descriptor), else plain pread through a pinned bounce buffer.
+class device_reader {
+public:
+    falcon_status open(const char* path) {
+        fd_ = ::open(path, O_RDONLY);
+        if (fd_ < 0) return set_error(FALCON_ERR_IO, std::string("cannot open ") + path);
+        struct stat st {};
+        if (::fstat(fd_, &st) != 0) return set_error(FALCON_ERR_IO, std::string("cannot stat ") + path);
+        size_ = (uint64_t)st.st_size;
+        const cufile_api& cf = cufile();
+        if (cf.ok) {
+            dfd_ = ::open(path, O_RDONLY | O_DIRECT);
+            for (int fd : {dfd_, fd_}) {
+                if (fd < 0) continue;
+                CUfileDescr_t d{};
+                d.type = CU_FILE_HANDLE_TYPE_OPAQUE_FD;
+                d.handle.fd = fd;
+                if (cf.handle_register(&fh_, &d).err == CU_FILE_SUCCESS) {
+                    gds_ = registered_ = true;
+                    break;
+                }
+            }
+        }
+        return FALCON_OK;
+    }
+    ~device_reader() {
+        if (registered_) cufile().handle_deregister(fh_);
+        if (dfd_ >= 0) ::close(dfd_);
+        if (fd_ >= 0) ::close(fd_);
+    }
+    uint64_t size() const { return size_; }
+    bool gds() const { return gds_; }
+
+    // bytes [off, off + n) of the file into device memory d
+    falcon_status read(uint64_t off, void* d, uint64_t n, pinned_buffer& bounce, cudaStream_t st) {
+        uint8_t* dst = static_cast<uint8_t*>(d);
+        if (gds_) {
+            uint64_t done = 0;
+            while (done < n) {
+                const ssize_t r = cufile().read(fh_, dst, n - done, (off_t)(off + done), (off_t)done);
+                if (r <= 0) {
+                    gds_ = false;   // the rest through the bounce buffer
+                    break;
+                }
+                done += (uint64_t)r;
+            }
+            if (done == n) return FALCON_OK;
+            off += done;
+            dst += done;
+            n -= done;
+        }
+        const uint64_t piece = 64ull << 20;
+        FB_TRY(bounce.ensure(2 * piece));
+        for (uint64_t done = 0, k = 0; done < n; ++k) {
+            const uint64_t len = std::min<uint64_t>(piece, n - done);
+            uint8_t* hb = bounce.as<uint8_t>() + (k & 1) * piece;
+            FB_CUDA(cudaStreamSynchronize(st));   // the half being refilled is no longer in flight
+            uint64_t got = 0;
+            while (got < len) {
+                const ssize_t r = ::pread(fd_, hb + got, len - got, (off_t)(off + done + got));
+                if (r <= 0) return set_error(FALCON_ERR_IO, "short read");
+                got += (uint64_t)r;
+            }
+            FB_CUDA(cudaMemcpyAsync(dst + done, hb, len, cudaMemcpyHostToDevice, st));
+            done += len;
+        }
+        FB_CUDA(cudaStreamSynchronize(st));
+        return FALCON_OK;
+    }
+
+private:
+    int fd_ = -1, dfd_ = -1;
+    uint64_t size_ = 0;
+    bool gds_ = false, registered_ = false;
+    CUfileHandle_t fh_ = nullptr;
+};
+
+falcon_status pwrite_all(int fd, const void* p, uint64_t n, uint64_t off) {
+    const uint8_t* c = static_cast<const uint8_t*>(p);
+    while (n) {
+        const ssize_t w = ::pwrite(fd, c, n, (off_t)off);
+        if (w <= 0) return set_error(FALCON_ERR_IO, "write failed");
+        c += w;
+        off += (uint64_t)w;
+        n -= (uint64_t)w;
+    }
+    return FALCON_OK;
+}
+
+struct fd_closer {
+    int fd;
+    ~fd_closer() {
+        if (fd >= 0) ::close(fd);
+    }
+};
+
+// whole batches per window: ~512 MiB of values
+uint64_t window_batches(uint64_t bv, size_t esz) {
+    const uint64_t b = (512ull << 20) / (bv * esz);
+    return b ? b : 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+falcon_status falcon_compress_file(falcon_ctx* ctx, int precision, const char* raw_path, const char* archive_path,
+                                   const falcon_pipeline_options* opt, uint64_t* archive_bytes, int* io_path) {
+    FB_NVTX("falcon_compress_file");
+    if (!ctx || !raw_path || !archive_path) return set_error(FALCON_ERR_INVALID, "null argument");
+    falcon_pipeline_options o;
+    falcon_default_options(&o);
+    if (opt) o = *opt;
+    FB_TRY(validate_options(o.chunk_n, o.batch_values));
+    const size_t esz = lane_bytes(precision);
+    device_guard dg(ctx->device);
+    device_reader in;
+    FB_TRY(in.open(raw_path));
+    if (in.size() % esz) return set_error(FALCON_ERR_IO, "input ends inside a value");
+    const uint64_t n = in.size() / esz, bv = o.batch_values;
+    const uint64_t wb = window_batches(bv, esz), wv = wb * bv;
+    const int ofd = ::open(archive_path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+    if (ofd < 0) return set_error(FALCON_ERR_IO, std::string("cannot open ") + archive_path);
+    fd_closer oc{ofd};
+    cudaStream_t st = nullptr;
+    FB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct stream_closer {
+        cudaStream_t s;
+        ~stream_closer() { cudaStreamDestroy(s); }
+    } sc{st};
+    device_buffer d_in, d_out, d_total_buf;
+    pinned_buffer bounce, h_out;
+    FB_TRY(d_total_buf.ensure(64));
+    const uint64_t first_window = std::min(n, wv);
+    FB_TRY(d_in.ensure(std::max<uint64_t>(first_window, 1) * esz));
+    const uint64_t obound = falcon_compress_bound(precision, first_window, o.chunk_n, bv);
+    FB_TRY(d_out.ensure(obound));
+    FB_TRY(h_out.ensure(obound));
+    uint64_t cursor = 47;
+    for (uint64_t v0 = 0; v0 < n; v0 += wv) {
+        const uint64_t cnt = std::min(wv, n - v0);
+        FB_TRY(in.read(v0 * esz, d_in.p, cnt * esz, bounce, st));
+        // the window's frames (no header: header_bytes 0) through the device codec
+        uint64_t* d_total = d_total_buf.as<uint64_t>();
+        FB_TRY(falcon_compress_device_frames(ctx, precision, d_in.p, cnt, o.chunk_n, bv, d_out.p, obound, d_total,
+                                             st));
+        uint64_t frames = 0;
+        FB_CUDA(cudaMemcpyAsync(&frames, d_total, 8, cudaMemcpyDeviceToHost, st));
+        FB_CUDA(cudaStreamSynchronize(st));
+        FB_TRY(falcon_ctx_sync(ctx, st));
+        FB_CUDA(cudaMemcpyAsync(h_out.p, d_out.p, frames, cudaMemcpyDeviceToHost, st));
+        FB_CUDA(cudaStreamSynchronize(st));
+        FB_TRY(pwrite_all(ofd, h_out.p, frames, cursor));
+        cursor += frames;
+    }
+    falcon_archive_info h{(uint8_t)precision, o.chunk_n, bv, n, (n + bv - 1) / bv};
+    uint8_t hdr[47];
+    falcon_write_header(&h, hdr);
+    FB_TRY(pwrite_all(ofd, hdr, 47, 0));
+    if (archive_bytes) *archive_bytes = cursor;
+    if (io_path) *io_path = in.gds() ? 1 : 0;
+    return FALCON_OK;
+}
+
+falcon_status falcon_decompress_file(falcon_ctx* ctx, int precision, const char* archive_path, const char* raw_path,
+                                     const falcon_pipeline_options* opt, uint64_t* n_values, int* io_path) {
+    FB_NVTX("falcon_decompress_file");
+    (void)opt;
+    if (!ctx || !raw_path || !archive_path) return set_error(FALCON_ERR_INVALID, "null argument");
+    device_guard dg(ctx->device);
+    device_reader in;
+    FB_TRY(in.open(archive_path));
+    const uint64_t len = in.size();
+    cudaStream_t st = nullptr;
+    FB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct stream_closer {
+        cudaStream_t s;
+        ~stream_closer() { cudaStreamDestroy(s); }
+    } sc{st};
+    // the whole archive into HBM (it is ~1/8 of the values), then its frames are indexed on
+    // the device (read_batch chain, container.cpp:113-132)
+    device_buffer d_arc;
+    pinned_buffer bounce;
+    FB_TRY(d_arc.ensure(std::max<uint64_t>(len, 64)));
+    FB_TRY(in.read(0, d_arc.p, len, bounce, st));
+    uint8_t hb[47] = {0};
+    const uint64_t hl = std::min<uint64_t>(len, 47);
+    if (hl) FB_CUDA(cudaMemcpy(hb, d_arc.p, hl, cudaMemcpyDeviceToHost));
+    falcon_archive_info h;
+    FB_TRY(falcon_read_header(hb, len, &h));
+    if (h.precision != precision)
+        return set_error(FALCON_ERR_INVALID, "archive precision does not match the requested value type");
+    const size_t esz = lane_bytes(precision);
+    const int ofd = ::open(raw_path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+    if (ofd < 0) return set_error(FALCON_ERR_IO, std::string("cannot open ") + raw_path);
+    fd_closer oc{ofd};
+    if (h.batch_count) {
+        device_buffer d_idx, d_vals;
+        FB_TRY(d_idx.ensure((h.batch_count + 1) * 8));
+        FB_TRY(falcon_archive_index(ctx, d_arc.p, len, &h, d_idx.as<uint64_t>(), st));
+        std::vector<uint64_t> idx(h.batch_count + 1);
+        FB_CUDA(cudaMemcpy(idx.data(), d_idx.p, idx.size() * 8, cudaMemcpyDeviceToHost));
+        if (idx[h.batch_count] != len) return set_error(FALCON_ERR_CORRUPT, "trailing bytes after final batch");
+        const uint64_t wb = window_batches(h.batch_values, esz);
+        const uint64_t wcap = std::min<uint64_t>(h.total_values, wb * h.batch_values);
+        FB_TRY(d_vals.ensure(std::max<uint64_t>(wcap, 1) * esz));
+        pinned_buffer h_vals;
+        FB_TRY(h_vals.ensure(std::max<uint64_t>(wcap, 1) * esz));
+        for (uint64_t b0 = 0; b0 < h.batch_count; b0 += wb) {
+            const uint64_t nb = std::min(wb, h.batch_count - b0);
+            uint64_t nv = 0;
+            FB_TRY(falcon_decompress_device_range(ctx, precision, d_arc.p, &h, idx.data(), b0, nb, d_vals.p, wcap,
+                                                  &nv, st));
+            FB_CUDA(cudaMemcpyAsync(h_vals.p, d_vals.p, nv * esz, cudaMemcpyDeviceToHost, st));
+            FB_CUDA(cudaStreamSynchronize(st));
+            FB_TRY(pwrite_all(ofd, h_vals.p, nv * esz, b0 * h.batch_values * esz));
+        }
+    } else if (len != 47) {
+        return set_error(FALCON_ERR_CORRUPT, "trailing bytes after final batch");
+    }
+    if (n_values) *n_values = h.total_values;
+    if (io_path) *io_path = in.gds() ? 1 : 0;
+    return FALCON_OK;
+}
+
+}  // extern "C"

@@ -31,6 +31,7 @@ EXPORTED = [
     "falcon_decompress_host", "falcon_compress_chunk", "falcon_decompress_chunk", "falcon_synth_fill",
     "falcon_ctx_set_kernel_events", "falcon_selftest_dp", "falcon_selftest_div",
     "falcon_synth_fill_at", "falcon_synth_device", "falcon_compress_host_multi", "falcon_decompress_host_multi",
+    "falcon_compress_device_frames", "falcon_compress_file", "falcon_decompress_file",
 ]
 
 
@@ -128,6 +129,11 @@ def load() -> C.CDLL:
                                              C.POINTER(u64), C.POINTER(PipelineStats)]
     L.falcon_decompress_host_multi.argtypes = [C.POINTER(vp), u32, i32, vp, u64, vp, u64, C.POINTER(u64),
                                                C.POINTER(PipelineOptions), C.POINTER(PipelineStats)]
+    L.falcon_compress_device_frames.argtypes = [vp, i32, vp, u64, u32, u64, vp, u64, vp, vp]
+    L.falcon_compress_file.argtypes = [vp, i32, C.c_char_p, C.c_char_p, C.POINTER(PipelineOptions),
+                                       C.POINTER(u64), C.POINTER(i32)]
+    L.falcon_decompress_file.argtypes = [vp, i32, C.c_char_p, C.c_char_p, C.POINTER(PipelineOptions),
+                                         C.POINTER(u64), C.POINTER(i32)]
     L.falcon_synth_fill_at.argtypes = [i32, C.POINTER(SynthSpec), u64, vp, u64]
     L.falcon_synth_device.argtypes = [vp, i32, C.POINTER(SynthSpec), u64, vp, u64, vp]
     L.falcon_default_options.argtypes = [C.POINTER(PipelineOptions)]
@@ -333,6 +339,20 @@ class Codec:
         _check(self.lib.falcon_synth_device(self.ctx, prec_of(out.dtype), C.byref(s), first,
                                             C.c_void_p(out.data_ptr()), out.numel(), st))
         return out
+
+    # ---- files through GPU-direct storage ----
+    def compress_file(self, raw_path: str, archive_path: str, prec: int = F64, opt: PipelineOptions | None = None):
+        """raw value file -> .fln archive; returns (archive bytes, io path: 1 cuFile / 0 bounce)."""
+        nb, io = C.c_uint64(), C.c_int32()
+        _check(self.lib.falcon_compress_file(self.ctx, prec, raw_path.encode(), archive_path.encode(),
+                                             C.byref(opt) if opt else None, C.byref(nb), C.byref(io)))
+        return nb.value, io.value
+
+    def decompress_file(self, archive_path: str, raw_path: str, prec: int = F64):
+        nv, io = C.c_uint64(), C.c_int32()
+        _check(self.lib.falcon_decompress_file(self.ctx, prec, archive_path.encode(), raw_path.encode(), None,
+                                               C.byref(nv), C.byref(io)))
+        return nv.value, io.value
 
     def set_kernel_events(self, enc=None, dec=None):
         """enc/dec: (start, stop) torch.cuda.Event pairs recorded around the main kernels."""

@@ -110,3 +110,22 @@ def test_two_processes_run_the_sharded_product(tmp_path, oracle):
     assert open(tmp_path / "ok.txt").read() == "True True"
     vals = synth("field", N_VALUES, F64, dp=2, seed=3)
     assert open(tmp_path / "global.fln", "rb").read() == oracle.compress_archive(vals, 1025, BV)
+
+
+# ---- files through GPU-direct storage (falcon_compress_file / falcon_decompress_file) ----
+@pytest.mark.parametrize("prec,kind", [(F64, "outlier"), (F32, "mixed")])
+def test_file_round_trip_through_gds(codec, oracle, tmp_path, prec, kind):
+    from paper_2511_04140_b200 import options as opts
+    vals = synth(kind, 33 * 1025 * 4 + 91, prec, seed=12, period=100)
+    raw, fln, back = tmp_path / "v.raw", tmp_path / "v.fln", tmp_path / "back.raw"
+    vals.tofile(raw)
+    nb, io = codec.compress_file(str(raw), str(fln), prec, opts(1025, 4 * 1025, 4, 0))
+    want = oracle.compress_archive(vals, 1025, 4 * 1025)
+    assert open(fln, "rb").read() == want and nb == len(want)
+    nv, io2 = codec.decompress_file(str(fln), str(back), prec)
+    assert nv == len(vals) and open(back, "rb").read() == vals.tobytes()
+    assert io in (0, 1) and io2 in (0, 1)
+    # a truncated archive fails like the reference
+    (tmp_path / "t.fln").write_bytes(want[:-9])
+    with pytest.raises(CorruptError):
+        codec.decompress_file(str(tmp_path / "t.fln"), str(tmp_path / "t.raw"), prec)
