@@ -36,6 +36,17 @@ constexpr size_t kEncTicket = 0, kEncError = 8, kEncTotal = 16, kDecTicket = 24,
 
 uint8_t* misc_at(falcon_ctx* ctx, size_t off) { return ctx->misc.as<uint8_t>() + off; }
 
+// A synchronous call reads its device error word and leaves it cleared, so a later
+// falcon_ctx_sync on the context does not report the same error again.
+falcon_status take_error(falcon_ctx* ctx, size_t off, cudaStream_t st, unsigned long long* err) {
+    uint8_t* hb = ctx->host_box.as<uint8_t>();
+    FB_CUDA(cudaMemcpyAsync(hb, misc_at(ctx, off), 8, cudaMemcpyDeviceToHost, st));
+    FB_CUDA(cudaMemsetAsync(misc_at(ctx, off), 0xff, 8, st));
+    FB_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(err, hb, 8);
+    return FALCON_OK;
+}
+
 falcon_status error_from_device(unsigned long long word, uint64_t cpb, bool batch_suffix,
                                 uint64_t first_batch = 0) {
     if (word == ~0ull) return FALCON_OK;
@@ -259,6 +270,7 @@ falcon_status falcon_compress_device(falcon_ctx* ctx, int precision, const void*
     slot_mailbox* box = ctx->host_box.as<slot_mailbox>();
     FB_CUDA(cudaMemcpyAsync(&box->total, misc_at(ctx, kEncTotal), 8, cudaMemcpyDeviceToHost, st));
     FB_CUDA(cudaMemcpyAsync(&box->error, misc_at(ctx, kEncError), 8, cudaMemcpyDeviceToHost, st));
+    FB_CUDA(cudaMemsetAsync(misc_at(ctx, kEncError), 0xff, 8, st));
     FB_CUDA(cudaStreamSynchronize(st));
     FB_TRY(error_from_device(box->error, g.cpb, false));
     if (box->total > out_cap)
@@ -315,9 +327,7 @@ falcon_status falcon_decompress_device(falcon_ctx* ctx, int precision, const voi
     geometry g;
     FB_TRY(enqueue_decompress(ctx, precision, d_archive, archive_bytes, &info, d_values, cap_values, st, g));
     unsigned long long err = ~0ull;
-    FB_CUDA(cudaMemcpyAsync(hb, misc_at(ctx, kDecError), 8, cudaMemcpyDeviceToHost, st));
-    FB_CUDA(cudaStreamSynchronize(st));
-    std::memcpy(&err, hb, 8);
+    FB_TRY(take_error(ctx, kDecError, st, &err));
     FB_TRY(error_from_device(err, g.cpb, true));
     if (n_values) *n_values = info.total_values;
     return FALCON_OK;
@@ -333,11 +343,8 @@ falcon_status falcon_archive_index(falcon_ctx* ctx, const void* d_archive, uint6
     FB_CUDA(cudaMemsetAsync(misc_at(ctx, kDecError), 0xff, 8, st));
     FB_CUDA(launch_index(static_cast<const uint8_t*>(d_archive), archive_bytes, 47, info->batch_count, d_index,
                          reinterpret_cast<unsigned long long*>(misc_at(ctx, kDecError)), st));
-    uint8_t* hb = ctx->host_box.as<uint8_t>();
-    FB_CUDA(cudaMemcpyAsync(hb, misc_at(ctx, kDecError), 8, cudaMemcpyDeviceToHost, st));
-    FB_CUDA(cudaStreamSynchronize(st));
     unsigned long long err;
-    std::memcpy(&err, hb, 8);
+    FB_TRY(take_error(ctx, kDecError, st, &err));
     return error_from_device(err, 1, true);  // keys are batch numbers
 }
 
@@ -377,11 +384,8 @@ falcon_status falcon_decompress_device_range(falcon_ctx* ctx, int precision, con
                         ? launch_decode<double>(arc, end - start, g, static_cast<double*>(d_values), ws, st)
                         : launch_decode<float>(arc, end - start, g, static_cast<float*>(d_values), ws, st);
     if (e != cudaSuccess) return set_error(FALCON_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
-    uint8_t* hb = ctx->host_box.as<uint8_t>();
-    FB_CUDA(cudaMemcpyAsync(hb, misc_at(ctx, kDecError), 8, cudaMemcpyDeviceToHost, st));
-    FB_CUDA(cudaStreamSynchronize(st));
     unsigned long long err;
-    std::memcpy(&err, hb, 8);
+    FB_TRY(take_error(ctx, kDecError, st, &err));
     return error_from_device(err, g.cpb, true, first_batch);
 }
 

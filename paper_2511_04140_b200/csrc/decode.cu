@@ -21,6 +21,8 @@
 #include "falcon_common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace fb200 {
 
 namespace {
@@ -171,7 +173,6 @@ __device__ uint64_t walk_frames_fast(const uint8_t* __restrict__ arc, uint64_t l
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nthreads = blockDim.x, nwarps = nthreads >> 5;
     __shared__ uint32_t s_wsum[32];
-    __shared__ int s_big;
     uint64_t cursor = g.header_bytes;
     *cursor_out = cursor;
     if ((((uintptr_t)arc) & 15) != 0 || (uint64_t)g.cpb + 8 > cap) return 0;
@@ -273,6 +274,240 @@ __device__ uint64_t walk_frames_fast(const uint8_t* __restrict__ arc, uint64_t l
     return b;
 }
 
+// Two-role fast walk (the common case: 16-B aligned archive, every frame as expected).
+// The serial chain of the walk is only "frame b's payload total -> frame b+1's position",
+// so the block splits:
+//   chain  (warps 0..7)   loads frame b's count + size table straight into registers
+//                         (16-B vectors), sums the table as rotated 32-bit words (the sum
+//                         of little-endian u32 entries at byte phase s is the sum of the
+//                         covering aligned words rotated right by 8s, edge words masked),
+//                         parks the vectors in one of two smem slots and moves on to frame
+//                         b+1 at once;
+//   writer (warps 8..15)  validates the entries, scans them into chunk offsets, stores
+//                         offsets/sizes and publishes the batch (barrier, fence, flag) off the
+//                         chain's critical path.
+// Slots hand over through mbarriers (FULL: chain -> writers, EMPTY: writers -> chain).
+// Either role stops at the first frame that is not exactly as expected (chain: count /
+// truncation; writer: an entry above the largest valid chunk); the general walker then
+// resumes at the first batch not published and reports the reference's error.
+constexpr int kChainThreads = 256;
+constexpr int kWalkPF = 5;  // vectors per chain thread: tables of up to 5108 entries
+constexpr uint32_t kWalkSlotBytes = kWalkPF * kChainThreads * 16 + 16;
+struct walk_slot_meta {
+    uint64_t cursor;  // frame position
+    uint64_t b;       // batch
+    uint32_t stop;    // 1: not a frame as expected, the walk ends at (b, cursor)
+};
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void wmbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void wmbar_arrive(uint64_t* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void wmbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(parity) : "memory");
+    }
+}
+
+// u32 at byte offset o (0..15) of the 32-byte window lo:hi (little endian)
+__device__ __forceinline__ uint32_t window_u32(const uint4& lo, const uint4& hi, uint32_t o) {
+    const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    const uint32_t q = o >> 2, sh = (o & 3) * 8;
+    uint32_t a = w[0], b = w[1];
+#pragma unroll
+    for (int i = 1; i < 4; ++i) {
+        a = q == (uint32_t)i ? w[i] : a;
+        b = q == (uint32_t)i ? w[i + 1] : b;
+    }
+    return __funnelshift_r(a, b, sh);
+}
+
+// Returns the first batch not published; *cursor_out = its frame position.  Needs 512
+// threads and walk_split_smem() bytes of dynamic smem.
+__host__ __device__ constexpr uint32_t walk_split_smem(uint32_t cpb) { return 2 * kWalkSlotBytes + 4 * cpb; }
+__device__ uint64_t walk_frames_split(const uint8_t* __restrict__ arc, uint64_t len, const geometry& g,
+                                      const decode_ws& ws, uint8_t* smem, uint32_t emax,
+                                      uint64_t* cursor_out) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    __shared__ walk_slot_meta s_meta[2];
+    __shared__ __align__(8) uint64_t s_full[2], s_empty[2];
+    __shared__ uint64_t s_csum[kChainThreads / 32];
+    __shared__ uint32_t s_wsum[kChainThreads / 32], s_wbig[kChainThreads / 32];
+    __shared__ uint64_t s_res_b, s_res_cursor;
+    __shared__ uint32_t s_wstop;  // the writer stopped (its resume point stands)
+    __shared__ uint32_t s_cok;
+    uint4* slots = reinterpret_cast<uint4*>(smem);
+    uint32_t* s_pref = reinterpret_cast<uint32_t*>(smem + 2 * kWalkSlotBytes);
+    if (tid == 0) {
+        s_wstop = 0;
+        s_res_b = g.n_batches;
+        s_res_cursor = 0;
+        for (int i = 0; i < 2; ++i) {
+            wmbar_init(&s_full[i], 1);
+            wmbar_init(&s_empty[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid < kChainThreads) {
+        // ============================ chain ============================
+        const int warp = tid >> 5;
+        uint64_t cursor = g.header_bytes;
+        for (uint64_t b = 0;; ++b) {
+            const int sl = (int)(b & 1);
+            // the slot's previous batch (b - 2) is done; a writer stop ends the chain
+            if (b >= 2) {
+                wmbar_wait(&s_empty[sl], (uint32_t)(((b - 2) >> 1) & 1));
+                if (atomicOr(&s_wstop, 0u)) break;
+            }
+            bool stop = b >= g.n_batches;
+            uint64_t next = 0;
+            if (!stop) {
+                const uint32_t exp = g.chunks_in(b);
+                const uint64_t v0 = cursor & ~15ull;
+                const uint32_t nvec = (uint32_t)(((cursor & 15) + 4 + 4 * (uint64_t)exp + 15) >> 4);
+                stop = len - cursor < 4 + 4 * (uint64_t)exp || len - v0 < 16ull * nvec;  // uniform
+                if (!stop) {
+                    const uint64_t tb = cursor + 4, te = tb + 4 * (uint64_t)exp;
+                    const uint32_t rs = (uint32_t)(tb & 3) * 8;
+                    uint4 pf[kWalkPF];
+#pragma unroll
+                    for (int k = 0; k < kWalkPF; ++k) {
+                        const uint32_t v = (uint32_t)tid + (uint32_t)k * kChainThreads;
+                        pf[k] = v < nvec ? __ldg(reinterpret_cast<const uint4*>(arc + v0 + 16ull * v)) : make_uint4(0, 0, 0, 0);
+                    }
+                    uint64_t sum = 0;
+#pragma unroll
+                    for (int k = 0; k < kWalkPF; ++k) {
+                        const uint64_t a = v0 + 16ull * ((uint32_t)tid + (uint32_t)k * kChainThreads);
+                        const uint32_t w4[4] = {pf[k].x, pf[k].y, pf[k].z, pf[k].w};
+                        if (a >= tb && a + 16 <= te) {
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) sum += __funnelshift_r(w4[q], w4[q], rs);
+                        } else if (a + 16 > tb && a < te) {  // edge vectors: mask bytes outside the table
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const uint64_t wa = a + 4 * q;
+                                const uint32_t lo = wa >= tb ? 0u : (uint32_t)min(tb - wa, (uint64_t)4);
+                                const uint32_t hi = wa >= te ? 0u : (uint32_t)min(te - wa, (uint64_t)4);
+                                const uint32_t m = hi > lo ? (uint32_t)(((1ull << (8 * hi)) - 1) & ~((1ull << (8 * lo)) - 1)) : 0u;
+                                sum += __funnelshift_r(w4[q] & m, w4[q] & m, rs);
+                            }
+                        }
+                    }
+                    sum = warp_sum_u64(sum);
+                    // the count word (bytes [cursor, cursor + 4)) lies in vectors 0 and 1
+                    const uint4 v1 = make_uint4(__shfl_sync(0xffffffffu, pf[0].x, 1), __shfl_sync(0xffffffffu, pf[0].y, 1),
+                                                __shfl_sync(0xffffffffu, pf[0].z, 1), __shfl_sync(0xffffffffu, pf[0].w, 1));
+                    if (lane == 0) s_csum[warp] = sum;
+                    uint4* dst = slots + (size_t)sl * (kWalkSlotBytes / 16);
+#pragma unroll
+                    for (int k = 0; k < kWalkPF; ++k) {
+                        const uint32_t v = (uint32_t)tid + (uint32_t)k * kChainThreads;
+                        if (v < nvec) dst[v] = pf[k];
+                    }
+                    named_sync(1, kChainThreads);
+                    uint64_t payload = 0;
+#pragma unroll
+                    for (int q = 0; q < kChainThreads / 32; ++q) payload += s_csum[q];
+                    // count (container.cpp:116) and payload truncation (:127-128)
+                    if (tid == 0) s_cok = window_u32(pf[0], v1, (uint32_t)(cursor & 15)) == exp && !(len - te < payload);
+                    named_sync(1, kChainThreads);
+                    stop = s_cok == 0;
+                    next = te + payload;
+                }
+            }
+            if (tid == 0) {
+                s_meta[sl].cursor = cursor;
+                s_meta[sl].b = b;
+                s_meta[sl].stop = stop ? 1u : 0u;
+                wmbar_arrive(&s_full[sl]);
+            }
+            if (stop) break;
+            cursor = next;
+        }
+    } else {
+        // ============================ writer ============================
+        const int wt = tid - kChainThreads, wwarp = wt >> 5;
+        for (uint64_t b = 0;; ++b) {
+            const int sl = (int)(b & 1);
+            wmbar_wait(&s_full[sl], (uint32_t)((b >> 1) & 1));
+            const walk_slot_meta m = s_meta[sl];
+            if (m.stop) {
+                if (wt == 0 && m.b <= s_res_b) {
+                    s_res_b = m.b;
+                    s_res_cursor = m.cursor;
+                }
+                break;
+            }
+            const uint32_t exp = g.chunks_in(b);
+            const uint32_t* W = reinterpret_cast<const uint32_t*>(slots + (size_t)sl * (kWalkSlotBytes / 16));
+            const uint32_t tbr = (uint32_t)(m.cursor & 15) + 4;  // table start in the slot
+            const uint32_t w0 = tbr >> 2, sh = (tbr & 3) * 8;
+            auto entry = [&](uint32_t i) -> uint32_t { return __funnelshift_r(W[w0 + i], W[w0 + i + 1], sh); };
+            const uint32_t per = (exp + kChainThreads - 1) / kChainThreads;
+            const uint32_t i0 = min(exp, (uint32_t)wt * per), i1 = min(exp, i0 + per);
+            uint32_t mine = 0, big = 0;
+            for (uint32_t i = i0; i < i1; ++i) {
+                const uint32_t e = entry(i);
+                big |= e > emax;
+                mine += e;
+            }
+            uint32_t incl = mine;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += t;
+            }
+            big = __reduce_or_sync(0xffffffffu, big);
+            if (lane == 31) {
+                s_wsum[wwarp] = incl;
+                s_wbig[wwarp] = big;
+            }
+            named_sync(2, kChainThreads);
+            uint32_t run = incl - mine, anybig = 0;
+#pragma unroll
+            for (int q = 0; q < kChainThreads / 32; ++q) {
+                run += q < wwarp ? s_wsum[q] : 0u;
+                anybig |= s_wbig[q];
+            }
+            if (anybig) {  // every entry <= emax keeps the u32 prefixes exact
+                if (wt == 0) {
+                    atomicOr(&s_wstop, 1u);
+                    s_res_b = b;
+                    s_res_cursor = m.cursor;
+                    wmbar_arrive(&s_empty[sl]);  // releases a chain waiting on this slot
+                }
+                break;
+            }
+            for (uint32_t i = i0; i < i1; ++i) {
+                s_pref[i] = run;
+                run += entry(i);
+            }
+            named_sync(2, kChainThreads);
+            const uint64_t pay0 = m.cursor + 4 + 4 * (uint64_t)exp;
+            const uint64_t first = b * g.cpb;
+            for (uint32_t i = wt; i < exp; i += kChainThreads) {
+                ws.chunk_off[first + i] = pay0 + s_pref[i];
+                ws.chunk_size[first + i] = entry(i);
+            }
+            named_sync(2, kChainThreads);
+            if (wt == 0) {  // barrier, fence, flag (see walk_frames); then the slot is free
+                __threadfence();
+                st_release32(&ws.ready[b], 1u);
+                wmbar_arrive(&s_empty[sl]);
+            }
+        }
+    }
+    __syncthreads();
+    *cursor_out = s_res_cursor;
+    return s_res_b;
+}
+
 }  // namespace
 
 // RN(g / p) for the Case-1 inverse scale (numeric.hpp:159-162) at alpha = 22 (beyond
@@ -321,6 +556,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+// shared loads at explicit 32-bit shared-window addresses: with smem[] indexing the
+// compiler rebuilt the window base ((CgaCtaId << 24) + offset) for every load (2 extra
+// ops per load in the gather).  The addresses depend on slot data read after the slot's
+// mbarrier wait, so the loads cannot be hoisted above it.
+// a value the compiler must keep in a register instead of rematerializing it
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
+    asm volatile("" : "+r"(x));
+    return x;
+}
+__device__ __forceinline__ uint32_t lds_u8_if(bool p, uint32_t a) {
+    uint32_t v = 0;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.u8 %0, [%1];\n\t}"
+        : "+r"(v) : "r"(a), "r"((uint32_t)p));
+    return v;
 }
 template <int NT>
 __device__ __forceinline__ void consumer_sync() {
@@ -373,7 +623,7 @@ struct __align__(16) slot_info {
 // and the sparse rows' bitmap popcounts (a chain over sparse rows only); for each
 // sparse row the consumer warps' payload prefixes are stored too.
 template <typename T, int NW, typename SI>
-__device__ __forceinline__ void parse_chunk(const uint8_t* p, const uint8_t* hp, uint32_t size, bool oversize,
+__device__ __forceinline__ void parse_chunk(uint32_t ps, const uint8_t* hp, uint32_t size, bool oversize,
                                             int NC, int BM, SI& si, int lane) {
     using tr = lane_traits<T>;
     using B = typename tr::B;
@@ -434,8 +684,8 @@ __device__ __forceinline__ void parse_chunk(const uint8_t* p, const uint8_t* hp,
                 if (size < rp + (uint32_t)BM) { bad = r; bad_code = DEV_E_BITMAP_TRUNC; break; }
                 // chain: one bitmap byte per lane, popcounts summed by REDUX (the next
                 // sparse row's offset needs only the total)
-                const uint32_t pa = lane < BM ? __popc(p[rp + lane]) : 0u;
-                const uint32_t pb = lane + 32 < BM ? __popc(p[rp + lane + 32]) : 0u;
+                const uint32_t pa = __popc(lds_u8_if(lane < BM, ps + rp + lane));
+                const uint32_t pb = __popc(lds_u8_if(lane + 32 < BM, ps + rp + lane + 32));
                 const uint32_t tot = __reduce_add_sync(0xffffffffu, pa + pb);
                 // off the chain: consumer warp q's payload prefix = popcounts of bitmap
                 // bytes [0, 4q) (exclusive scan of 4-byte group sums over lanes q < NW)
@@ -498,14 +748,16 @@ __device__ __forceinline__ void parse_chunk(const uint8_t* p, const uint8_t* hp,
 constexpr int kWalkThreads = 512;
 __global__ void __launch_bounds__(kWalkThreads) walker_kernel(const uint8_t* __restrict__ arc, uint64_t len_arg,
                                                               const uint64_t* __restrict__ d_len, geometry g,
-                                                              decode_ws ws, uint32_t cap, uint32_t emax) {
+                                                              decode_ws ws, uint32_t cap, uint32_t emax, bool split) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uint64_t len = d_len ? *d_len : len_arg;
     extern __shared__ __align__(16) uint8_t wsmem[];
     uint4* raw = reinterpret_cast<uint4*>(wsmem);                 // 4 cap + 32 bytes
     uint32_t* pref = reinterpret_cast<uint32_t*>(wsmem + 4 * (size_t)cap + 32);  // cap entries
     uint64_t cursor;
-    const uint64_t b0 = walk_frames_fast<4>(arc, len, g, ws, raw, pref, cap, emax, &cursor);
+    uint64_t b0;
+    if (split) b0 = walk_frames_split(arc, len, g, ws, wsmem, emax, &cursor);
+    else b0 = walk_frames_fast<4>(arc, len, g, ws, raw, pref, cap, emax, &cursor);
     walk_frames(arc, len, g, ws, raw, pref, cap, b0, cursor);
 }
 
@@ -619,7 +871,7 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers, decode_min
             if (kind != SLOT_EXIT) fetch(it + kProducers, t2, kind2, off2, size2);
             asm volatile("cp.async.wait_all;" ::: "memory");
             __syncwarp();
-            if (kind == SLOT_CHUNK) parse_chunk<T, nwarps>(buf + a, staged ? buf + a : arc + off, size, !staged, NC, BM, si, lane);
+            if (kind == SLOT_CHUNK) parse_chunk<T, nwarps>(opaque_u32(smem_u32(buf + a)), staged ? buf + a : arc + off, size, !staged, NC, BM, si, lane);
             if (lane == 0) {
                 si.kind = kind;
                 si.chunk = t;
@@ -677,7 +929,10 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers, decode_min
         } else if (kind == SLOT_CHUNK) {
             const uint64_t v0 = si.v0;
             const uint32_t count = si.count;
-            const uint8_t* img = smem + (size_t)sl * region + (uint32_t)(si.off & 15);
+            // the chunk's bytes as 32-bit offsets into smem[] (a generic img pointer made the
+            // compiler rebuild each load address from the shared window, 3 extra ops per load)
+            const uint32_t ib = opaque_u32(smem_u32(smem)) + (uint32_t)sl * region + (uint32_t)(si.off & 15);
+            const uint32_t icol = ib + (uint32_t)tid, ibm = ib + ((uint32_t)tid >> 3);
             const int w = (int)si.w;
             const uint32_t hA = si.hA;
             const bool case2 = hA > (uint32_t)tr::max_alpha;
@@ -703,7 +958,7 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers, decode_min
         uint32_t xb[8];
         if (dblk == 0xffu) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) xb[k] = active ? img[ro[k] + tid] : 0u;
+            for (int k = 0; k < 8; ++k) xb[k] = lds_u8_if(active, icol + ro[k]);
         } else {
             const uint4 wp = *reinterpret_cast<const uint4*>(&si.wpre[warp * 64 + 8 * sb]);
             const uint32_t wpre[8] = {wp.x & 0xffffu, wp.x >> 16, wp.y & 0xffffu, wp.y >> 16,
@@ -714,11 +969,11 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers, decode_min
                 xb[k] = 0u;
                 if (k >= kmax) continue;  // uniform: rows above w
                 const bool dk = (dblk >> k) & 1u;
-                const uint32_t bmb = (!dk && active) ? img[ro[k] + (tid >> 3)] : 0u;
+                const uint32_t bmb = lds_u8_if(!dk && active, ibm + ro[k]);
                 const uint32_t bit = (bmb >> bsh) & 1u;
                 const uint32_t m = __ballot_sync(0xffffffffu, bit);
-                const uint32_t idx = dk ? ro[k] + tid : ro[k] + BM + wpre[k] + __popc(m & lt_mask);
-                xb[k] = ((dk && active) || bit) ? img[idx] : 0u;
+                const uint32_t idx = dk ? icol + ro[k] : ib + ro[k] + BM + wpre[k] + __popc(m & lt_mask);
+                xb[k] = lds_u8_if((dk && active) || bit, idx);
             }
         }
         // byte k of x = row byte of plane 8sb+k (xb[k] <= 0xff: selector 7 reads a zero byte)
@@ -956,12 +1211,20 @@ cudaError_t launch_decode(const uint8_t* d_archive, uint64_t len, const geometry
     // walker smem: the whole size table of a batch when it fits (fast path), else segments
     uint32_t cap = g.cpb + 64 < (24u << 10) ? g.cpb + 64 : (24u << 10);
     cap = (cap + 3) & ~3u;
-    const size_t wsm = 8 * (size_t)cap + 48;
+    static const bool split_ok = std::getenv("FALCON_WALK_SERIAL") == nullptr;  // A/B knob
+    // the two-role walk when every table fits the chain's registers and the u32 prefixes
+    // of valid entries cannot wrap
+    const uint32_t emax0 = (uint32_t)(lane_traits<T>::header + (lane_traits<T>::width + 7) / 8 +
+                                      lane_traits<T>::width * ((g.chunk_n - 1) / 8));
+    const bool split = ((uintptr_t)d_archive & 15) == 0 && (uint64_t)g.cpb + 8 <= 4ull * kWalkPF * kChainThreads &&
+                       (uint64_t)g.cpb * emax0 < (1ull << 32) && split_ok;
+    size_t wsm = 8 * (size_t)cap + 48;
+    if (split && walk_split_smem(g.cpb) > wsm) wsm = walk_split_smem(g.cpb);
     if ((e = ensure_dynamic_smem((const void*)walker_kernel, (uint32_t)wsm))) return e;
     if (ev0 && (e = cudaEventRecord(ev0, st))) return e;
     const uint32_t emax = (uint32_t)(lane_traits<T>::header + (lane_traits<T>::width + 7) / 8 +
                                       lane_traits<T>::width * ((g.chunk_n - 1) / 8));  // max_encoded_chunk_size
-    walker_kernel<<<1, kWalkThreads, wsm, st>>>(d_archive, len, d_len, g, ws, cap, emax);
+    walker_kernel<<<1, kWalkThreads, wsm, st>>>(d_archive, len, d_len, g, ws, cap, emax, split);
     if ((e = cudaGetLastError())) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);

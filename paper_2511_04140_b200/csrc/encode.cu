@@ -183,6 +183,29 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     const uint32_t len = left < n ? (uint32_t)left : n;  // short final chunk: +0.0 padding
     const bool active = tid < NC;
 
+    // The chunk L.pf_ahead CTAs later (about one generation of resident CTAs) is pulled into
+    // L2 with one bulk prefetch, so its CTA's value loads hit L2 instead of waiting on DRAM
+    // (the load latency sits on every CTA's critical path: phase 1 cannot start without it).
+#ifndef FB_ENC_NO_PREFETCH
+    // (f64 only: cfg2 compress -1.2 %; f32 had no gain and its 32-register budget spilled)
+    if (sizeof(T) == 8 && tid == 0 && L.pf_ahead) {
+        uint32_t ci2 = ci + L.pf_ahead;
+        uint32_t b2 = b;
+        if (ci2 >= g.cpb) {
+            ci2 -= g.cpb;
+            ++b2;
+        }
+        if (ci2 < g.cpb && b2 < L.b_end && ci2 < g.chunks_in(b2)) {
+            const uint64_t s0 = ((uint64_t)b2 * g.batch_values + (uint64_t)ci2 * n) * sizeof(T);
+            const uint64_t e0 = min(s0 + (uint64_t)n * sizeof(T), g.n_values * sizeof(T));
+            const uint64_t s16 = s0 & ~15ull, e16 = e0 & ~15ull;
+            if (e16 > s16)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(in) + s16),
+                             "r"((uint32_t)(e16 - s16)) : "memory");
+        }
+    }
+#endif
+
     // ---- load: values 8t .. 8t+8 (pipeline.hpp:205-215 zero padding) ----
     T v[8];
     T vprev = T(0);
@@ -938,6 +961,11 @@ cudaError_t launch_encode(const T* d_in, const geometry& g, uint8_t* d_out, uint
         L.enc_slot0 = (uint32_t)((b0 * g.cpb) % w.ring);
         L.place_c0 = (uint32_t)(placed * w.tile);
         L.place_slot0 = (uint32_t)((placed * w.tile) % w.ring);
+        L.b_end = (uint32_t)(b0 + nb);
+        // A/B knob FALCON_ENC_PREFETCH = distance in chunks (0: off)
+        static const char* pfe = std::getenv("FALCON_ENC_PREFETCH");
+        static const uint32_t pf = pfe ? (uint32_t)std::strtoul(pfe, nullptr, 10) : 768u;
+        L.pf_ahead = pf;
         if (nb == 0 && L.place_tiles == 0) continue;
         if (nb == 0) {
             e = launch_place_final(threads, L.place_tiles, g, d_out, out_cap, ws, L, hdr, st);

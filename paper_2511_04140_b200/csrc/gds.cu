@@ -3,8 +3,8 @@
 // cuFile's own compat path where the nvidia-fs driver is absent), compressed by the
 // device-resident codec in windows of whole batches, and the frames written out; the
 // inverse reads the archive into HBM, indexes its frames on the device and decodes batch
-// windows into the raw file.  libcufile is loaded with dlopen: without it (or on a file
-// system cuFile cannot register) reads go through a pinned bounce buffer instead.
+// windows into the raw file.  libcufile is loaded with dlopen when FALCON_CUFILE=1: without
+// it (or on a file system cuFile cannot register) reads go through a pinned bounce buffer.
 #include <cufile.h>
 #include <dlfcn.h>
 #include <fcntl.h>
@@ -30,7 +30,10 @@ struct cufile_api {
 const cufile_api& cufile() {
     static const cufile_api api = [] {
         cufile_api a;
-        if (std::getenv("FALCON_NO_CUFILE")) return a;
+        // opt-in: on the pool's B200 boxes (no nvidia-fs) a cuFile call hung the GPU test
+        // run past its time limit (profiles/r02), so the pinned bounce path is the default
+        const char* on = std::getenv("FALCON_CUFILE");
+        if (!on || on[0] != '1' || std::getenv("FALCON_NO_CUFILE")) return a;
         void* h = dlopen("libcufile.so.0", RTLD_NOW | RTLD_LOCAL);
         if (!h) h = dlopen("libcufile.so", RTLD_NOW | RTLD_LOCAL);
         if (!h) return a;

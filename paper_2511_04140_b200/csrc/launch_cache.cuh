@@ -18,9 +18,11 @@ inline std::mutex& lock() {
 }
 }  // namespace launch_cache_detail
 
-// raise the kernel's dynamic shared memory limit to at least `bytes` (only grows)
+// raise the kernel's dynamic shared memory limit to at least `bytes` (only grows).  The
+// 48 KB default bounds static + dynamic smem together, so there is no shortcut below it
+// (a 47 KB walker launch beside 1 KB of static smem failed with "invalid argument").
 inline cudaError_t ensure_dynamic_smem(const void* kern, uint32_t bytes) {
-    if (bytes <= 48u * 1024u) return cudaSuccess;     // below the default limit
+    if (bytes <= 16u * 1024u) return cudaSuccess;     // + static smem stays below 48 KB
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e) return e;

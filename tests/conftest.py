@@ -12,6 +12,15 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA product path)")
 
 
+def pytest_collection_modifyitems(config, items):
+    # a hung test fails on its own instead of eating the whole run's time limit
+    if not config.pluginmanager.hasplugin("timeout"):
+        return
+    for it in items:
+        if it.get_closest_marker("timeout") is None:
+            it.add_marker(pytest.mark.timeout(600 if it.get_closest_marker("gpu") else 900))
+
+
 @pytest.fixture(scope="session")
 def oracle():
     from oracle.oracle import Oracle

@@ -146,3 +146,19 @@ def test_random_corruption_fuzz_matches_oracle(codec, oracle, kind, prec):
             with pytest.raises(FalconError) as ei:
                 codec.decompress_device(t, len(a))
             assert str(ei.value) == want_msg, f"trial {trial}"
+
+
+def test_sync_error_does_not_leak_into_the_next_call(codec, oracle):
+    # a synchronous call that fails leaves its device error word cleared: the next call on
+    # the same context (and falcon_ctx_sync) reports only its own outcome
+    vals = synth("outlier", 1025 * 8 + 7, F64, seed=21, period=100)
+    arc = oracle.compress_archive(vals, 1025, 1025 * 4)
+    bad = torch.frombuffer(bytearray(arc[:-9]), dtype=torch.uint8).cuda()
+    with pytest.raises(CorruptError):
+        codec.decompress_device(bad, len(arc) - 9)
+    d = torch.from_numpy(vals).cuda()
+    got, nb = codec.compress_device(d, chunk_n=1025, batch_values=1025 * 4)
+    assert got[:nb].cpu().numpy().tobytes() == arc
+    codec.sync()
+    back = codec.decompress_device(got, nb).cpu().numpy()
+    assert bits(back) == bits(vals)
