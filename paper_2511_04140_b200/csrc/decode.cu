@@ -583,8 +583,8 @@ __device__ __forceinline__ void consumer_sync() {
 template <typename T> struct decode_cfg { static constexpr int producers = 2, slots = 4; };
 // f32 at the default chunk size: 6 resident blocks of 192 threads (56 registers; A/B: vs no
 // bound -0.3 %, vs a 1-block bound (62 registers, 5 blocks) -3 %, vs 7 / 8 blocks, which
-// spill, -2 % / -1 %).  f64 (0 = no bound) allocates 56
-// registers by itself; the slot ring allows 6 f64 blocks per SM anyway.
+// spill, -2 % / -1 %).  f64 (0 = no bound) allocates 56 registers or fewer by itself; the
+// slot ring allows 6 f64 blocks per SM anyway.
 template <typename T, int NT>
 constexpr int decode_min_blocks() { return sizeof(T) == 4 && NT <= 128 ? 6 : 0; }
 static_assert(decode_cfg<double>::slots % decode_cfg<double>::producers == 0, "slot reuse");
@@ -884,9 +884,9 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers, decode_min
                     const uint64_t left = g.values_in(b) - (uint64_t)ci * n;
                     si.v0 = (uint64_t)b * g.batch_values + (uint64_t)ci * n;
                     si.count = left < n ? (uint32_t)left : n;
-                    const T sc = pow10_of(T{}, si.hA > (uint32_t)tr::max_alpha ? 0 : (int)si.hA);
-                    si.scale = sc;
-                    si.rscale = div_rn(T(1), sc);
+                    const int al = si.hA > (uint32_t)tr::max_alpha ? 0 : (int)si.hA;
+                    si.scale = pow10_of(T{}, al);
+                    si.rscale = rpow10_of(T{}, al);   // RN(1 / 10^alpha), host-computed table
                 }
             }
             __syncwarp();

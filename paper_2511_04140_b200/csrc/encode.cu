@@ -175,12 +175,16 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     }
     const uint32_t b = L.b0 + blockIdx.y - 1;
     const uint32_t ci = blockIdx.x;
-    if (b >= g.n_batches || ci >= g.chunks_in(b)) return;  // uniform per CTA
+    uint32_t len = n;
+    if (b >= L.full_b) {  // the last batch / short chunks: bounds and the chunk length
+        if (b >= g.n_batches || ci >= g.chunks_in(b)) return;  // uniform per CTA
+        const uint64_t left = g.values_in(b) - (uint64_t)ci * n;
+        len = left < n ? (uint32_t)left : n;  // short final chunk: +0.0 padding
+    } else if (ci >= g.cpb) {
+        return;
+    }
     const uint32_t c = b * g.cpb + ci;                      // < 2^31 chunks per launch
-    const uint64_t bcount = g.values_in(b);
     const uint64_t v0 = (uint64_t)b * g.batch_values + (uint64_t)ci * n;
-    const uint64_t left = bcount - (uint64_t)ci * n;
-    const uint32_t len = left < n ? (uint32_t)left : n;  // short final chunk: +0.0 padding
     const bool active = tid < NC;
 
     // The chunk L.pf_ahead CTAs later (about one generation of resident CTAs) is pulled into
@@ -229,6 +233,7 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     //      largest sampled alpha (attained, so alpha_max >= A0); lane 0 also prepares
     //      the chunk-uniform certification parameters for everybody ----
     __shared__ cert_params<T> s_cp;
+    __shared__ uint32_t s_lim;   // f64 narrow-path bound for 10^A0 (used when alpha_max == A0)
     if (warp == 0) {
         const int a = dp_alpha_k<T, 4>(v[3]);
         const uint32_t f1 = __reduce_or_sync(0xffffffffu, a < 0 ? 0x80000000u : (1u << a));
@@ -236,6 +241,7 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
             s_flag1[0] = f1;
             const int a0 = (f1 & 0x7fffffffu) ? 31 - __clz((int)(f1 & 0x7fffffffu)) : 0;
             s_cp = cert_params_for(T{}, a0);
+            s_lim = (2074u - ((uint32_t)__double2hiint((double)X::pow10(a0)) >> 20)) << 20;
         }
     }
     __syncthreads();
@@ -343,8 +349,8 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     // would miss a wide value there (transform.hpp:87-88 wraps in 64 bits).
     const T scale = X::pow10(case2 ? 0 : amax);
     const bool reuse = !case2 && amax == A0;
-    const uint32_t lim = (2074u - ((uint32_t)__double2hiint((double)scale) >> 20)) << 20;
-    const bool narrow = sizeof(B) == 8 && reuse && M < lim;
+    // (reuse: scale = 10^A0, whose bound phase 1 computed)
+    const bool narrow = sizeof(B) == 8 && reuse && M < s_lim;
     B z[8];
     B orv = 0;
     if (narrow) {
@@ -962,6 +968,7 @@ cudaError_t launch_encode(const T* d_in, const geometry& g, uint8_t* d_out, uint
         L.place_c0 = (uint32_t)(placed * w.tile);
         L.place_slot0 = (uint32_t)((placed * w.tile) % w.ring);
         L.b_end = (uint32_t)(b0 + nb);
+        L.full_b = g.batch_values % g.chunk_n == 0 && g.n_batches ? (uint32_t)(g.n_batches - 1) : 0u;
         // A/B knob FALCON_ENC_PREFETCH = distance in chunks (0: off)
         static const char* pfe = std::getenv("FALCON_ENC_PREFETCH");
         static const uint32_t pf = pfe ? (uint32_t)std::strtoul(pfe, nullptr, 10) : 768u;

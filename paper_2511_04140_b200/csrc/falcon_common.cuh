@@ -65,6 +65,8 @@ template <> struct lane_traits<float> {
 #endif
 FB_TABLE_SPACE double g_pow10_f64[23];
 FB_TABLE_SPACE float g_pow10_f32[11];
+FB_TABLE_SPACE double g_rpow10_f64[23];      // RN(1 / 10^a)
+FB_TABLE_SPACE float g_rpow10_f32[11];
 FB_TABLE_SPACE uint64_t g_decade_f64[618];  // + guard entry (+inf) for exponent 0x7ff
 FB_TABLE_SPACE uint32_t g_decade_f32[78];   // + guard entry (+inf) for exponent 0xff
 #endif
@@ -98,6 +100,8 @@ __device__ __forceinline__ float value_of(uint32_t b) { return __uint_as_float(b
 
 __device__ __forceinline__ double pow10_of(double, int a) { return g_pow10_f64[a]; }
 __device__ __forceinline__ float pow10_of(float, int a) { return g_pow10_f32[a]; }
+__device__ __forceinline__ double rpow10_of(double, int a) { return g_rpow10_f64[a]; }
+__device__ __forceinline__ float rpow10_of(float, int a) { return g_rpow10_f32[a]; }
 
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }

@@ -34,6 +34,7 @@ struct encode_launch {
     uint32_t enc_c0, enc_slot0;       // first chunk encoded here and its ring slot
     uint32_t place_c0, place_slot0;   // first chunk placed here and its ring slot
     uint32_t b_end;                   // first batch after this launch's wave
+    uint32_t full_b;                  // batches [0, full_b) hold cpb full chunks each
     uint32_t pf_ahead;                // L2 prefetch distance in chunks (0: off)
 };
 template <typename T> uint32_t encode_slot_bytes(uint32_t chunk_n);

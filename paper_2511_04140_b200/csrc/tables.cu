@@ -20,6 +20,12 @@ cudaError_t upload_tables() {
     for (int i = 0; i < 23; ++i, d *= 10.0) p64[i] = d;
     float f = 1.0f;
     for (int i = 0; i < 11; ++i, f *= 10.0f) p32[i] = f;
+    // RN(1 / 10^a), the decoder's division-free inverse scale (dpds.cuh): IEEE division on
+    // the host, correctly rounded like the device's div_rn
+    double r64[23];
+    float r32[11];
+    for (int i = 0; i < 23; ++i) r64[i] = 1.0 / p64[i];
+    for (int i = 0; i < 11; ++i) r32[i] = 1.0f / p32[i];
     uint64_t dec64[618];
     uint32_t dec32[78];
     dec64[617] = 0x7ff0000000000000ull;  // guard: only read for inf/nan lanes
@@ -38,6 +44,8 @@ cudaError_t upload_tables() {
     cudaError_t e;
     if ((e = cudaMemcpyToSymbol(g_pow10_f64, p64, sizeof p64))) return e;
     if ((e = cudaMemcpyToSymbol(g_pow10_f32, p32, sizeof p32))) return e;
+    if ((e = cudaMemcpyToSymbol(g_rpow10_f64, r64, sizeof r64))) return e;
+    if ((e = cudaMemcpyToSymbol(g_rpow10_f32, r32, sizeof r32))) return e;
     if ((e = cudaMemcpyToSymbol(g_decade_f64, dec64, sizeof dec64))) return e;
     return cudaMemcpyToSymbol(g_decade_f32, dec32, sizeof dec32);
 }
