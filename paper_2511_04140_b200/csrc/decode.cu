@@ -438,7 +438,9 @@ __device__ uint64_t walk_frames_split(const uint8_t* __restrict__ arc, uint64_t 
             wmbar_wait(&s_full[sl], (uint32_t)((b >> 1) & 1));
             const walk_slot_meta m = s_meta[sl];
             if (m.stop) {
-                if (wt == 0 && m.b <= s_res_b) {
+                // (a writer that stopped by itself left the loop before any stop marker; no
+                // read of s_res here: the other writers would race with this write)
+                if (wt == 0) {
                     s_res_b = m.b;
                     s_res_cursor = m.cursor;
                 }
