@@ -219,9 +219,11 @@ falcon_status falcon_decompress_host_multi(falcon_ctx* const* ctxs, unsigned n_c
                                            falcon_pipeline_stats* stats);
 
 /* ---- files through GPU-direct storage ----
- * Raw value files are read straight into device memory with cuFile (GPUDirect Storage,
- * or cuFile's compat path) when libcufile is present, else through a pinned bounce
- * buffer; *io_path (optional) gets 1 for cuFile, 0 for the bounce path.  Compress runs the
+ * Raw value files are read into device memory through a pinned double buffer (pread +
+ * async H2D), or with cuFile (GPUDirect Storage, or cuFile's compat path) when the
+ * environment sets FALCON_CUFILE=1 and libcufile loads -- opt-in because cuFileDriverOpen()
+ * hung on hosts without nvidia-fs.  *io_path (optional) gets 1 for cuFile, 0 for the
+ * bounce path.  Compress runs the
  * device codec over windows of whole batches and writes frames, then the header: the
  * archive equals falcon_compress_host's.  Decompress reads the archive into HBM, indexes
  * its frames on the device and decodes batch windows into the raw file. */

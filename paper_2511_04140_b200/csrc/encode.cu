@@ -128,7 +128,7 @@ template <typename T, int NT>
 constexpr int encode_min_blocks() {
     return NT <= 128 ? (sizeof(T) == 4 ? FB_ENC_MIN_BLOCKS32 : FB_ENC_MIN_BLOCKS) : (2048 / NT > 0 ? 2048 / NT : 1);
 }
-template <int NT, int U>
+template <int NT, int U, int NTHR = NT>
 __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_t out_cap, const encode_ws& ws,
                            const encode_launch& L, const archive_header_bytes& hdr, uint8_t* smem);
 
@@ -591,16 +591,23 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
 // size-table entries (container.cpp:88-111), copies each image to
 // chunk_base(c) + exclusive prefix with funnel-shifted 16-B stores, and the first
 // tile writes the 47-byte header (container.cpp:44-55).
-template <int NT, int U>
+// NTHR threads (a multiple of NT): threads [0, NT) scan the tile, and the copy is spread
+// over all NTHR / 32 warps, each moving NT * 32 / NTHR chunks (the final placement runs with
+// more threads than chunks: with 32 chunks per warp a small input was a chain of dependent
+// round trips per lane).
+template <int NT, int U, int NTHR>
 __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_t out_cap, const encode_ws& ws,
                            const encode_launch& L, const archive_header_bytes& hdr, uint8_t* smem) {
     constexpr int kPlaceTile = NT;
+    static_assert(NTHR % NT == 0 && NTHR <= 1024, "placement threads");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int NW = kPlaceTile / 32;
+    constexpr int NW = kPlaceTile / 32;     // scan warps
+    constexpr int NCW = NTHR / 32;          // copy warps
+    constexpr int CPW = NT / NCW;           // chunks per copy warp (<= 32)
     // carved from the encode kernel's dynamic smem (placement_smem_bytes)
     uint64_t* s_off = reinterpret_cast<uint64_t*>(smem);                       // [NT]
     uint32_t* s_sz = reinterpret_cast<uint32_t*>(s_off + kPlaceTile);          // [NT]
-    uint32_t (*s_vpre)[33] = reinterpret_cast<uint32_t (*)[33]>(s_sz + kPlaceTile);  // [NW][33]
+    uint32_t (*s_vpre)[33] = reinterpret_cast<uint32_t (*)[33]>(s_sz + kPlaceTile);  // [NCW][33]
     __shared__ uint32_t s_ticket;
     __shared__ uint32_t s_wsum[NW];
     __shared__ uint64_t s_tile_excl;
@@ -608,7 +615,7 @@ __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_
     __syncthreads();
     const uint64_t t = s_ticket;
     const uint64_t c = t * kPlaceTile + tid;
-    const bool valid = c < g.n_chunks;
+    const bool valid = tid < kPlaceTile && c < g.n_chunks;
     const uint32_t sz = valid ? ws.sizes[c] : 0u;
 
     // tile-local exclusive scan (a tile holds < 2^32 bytes)
@@ -618,7 +625,7 @@ __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_
         const uint32_t x = __shfl_up_sync(0xffffffffu, incl, d);
         if (lane >= d) incl += x;
     }
-    if (lane == 31) s_wsum[warp] = incl;
+    if (lane == 31 && warp < NW) s_wsum[warp] = incl;
     __syncthreads();
     uint32_t wbase = 0, tile_sum = 0;
 #pragma unroll
@@ -654,8 +661,10 @@ __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_
     }
     __syncthreads();
     const uint64_t pexcl = s_tile_excl + wbase + (incl - sz);  // payload bytes before chunk c
-    s_off[tid] = valid ? g.chunk_base(c) + pexcl : 0;
-    s_sz[tid] = sz;
+    if (tid < kPlaceTile) {
+        s_off[tid] = valid ? g.chunk_base(c) + pexcl : 0;
+        s_sz[tid] = sz;
+    }
 
     if (valid) {
         const uint64_t b = g.batch_of(c);
@@ -700,14 +709,14 @@ __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_
         for (int i = 0; i < 47; ++i) out[i] = hdr.b[i];
     }
 
-    // copy: each warp moves its 32 chunks as one flat list of destination vectors, so a
+    // copy: each warp moves its CPW chunks as one flat list of destination vectors, so a
     // lane's consecutive vectors are independent (their loads overlap) instead of the
     // chunks being copied one after another
     {
-        const int idx = warp * 32 + lane;
+        const int idx = warp * CPW + lane;
         const uint64_t cc = t * kPlaceTile + idx;
         uint32_t nv = 0;
-        if (cc < g.n_chunks) {
+        if (lane < CPW && cc < g.n_chunks) {
             const uint64_t off = s_off[idx];
             const uint32_t size = s_sz[idx];
             if (off + size > out_cap) record_error(ws.error, cc, DEV_E_CAPACITY);
@@ -719,11 +728,11 @@ __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_
             const uint32_t x = __shfl_up_sync(0xffffffffu, incl, d);
             if (lane >= d) incl += x;
         }
-        s_vpre[warp][lane] = incl - nv;
-        if (lane == 31) s_vpre[warp][32] = incl;
+        if (lane < CPW) s_vpre[warp][lane] = incl - nv;
+        if (lane == 31) s_vpre[warp][CPW] = incl;             // the warp's total
         __syncwarp();
     }
-    const uint32_t V = s_vpre[warp][32];
+    const uint32_t V = s_vpre[warp][CPW];
     int k = 0;  // this lane's current chunk (vectors are visited in increasing order)
     // U vectors per lane in flight: all their loads are issued before the first store
     // (a lane's copy is otherwise a chain of ~V/32 dependent DRAM round trips)
@@ -740,7 +749,7 @@ __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_
             from[u] = to[u] = 0;
             if (gv >= V) continue;
             while (gv >= s_vpre[warp][k + 1]) ++k;
-            const int idx = warp * 32 + k;
+            const int idx = warp * CPW + k;
             const uint64_t cc = t * kPlaceTile + idx;
             const uint64_t off = s_off[idx];
             uint32_t rs = L.place_slot0 + (uint32_t)(cc - L.place_c0);   // = cc mod ring
@@ -781,12 +790,12 @@ __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_
     // are whole 128-B lines, encode_slot_bytes); lane L discards lines L, L + 32, ...
     __syncwarp();
     for (int q = 0; q < 32; ++q) {
-        const uint64_t cc = t * kPlaceTile + warp * 32 + q;
-        if (cc >= g.n_chunks) break;
+        const uint64_t cc = t * kPlaceTile + warp * CPW + q;
+        if (q >= CPW || cc >= g.n_chunks) break;
         uint32_t rs = L.place_slot0 + (uint32_t)(cc - L.place_c0);
         rs = rs >= ws.ring ? rs - (uint32_t)ws.ring : rs;
         const uint8_t* img = ws.images + rs * (uint64_t)ws.slot;
-        const uint32_t lines = (s_sz[warp * 32 + q] + 4 + 127) >> 7;
+        const uint32_t lines = (s_sz[warp * CPW + q] + 4 + 127) >> 7;
         for (uint32_t ln = lane; ln < lines; ln += 32) l2_discard_line(img + 128 * ln);
     }
 #endif
@@ -794,11 +803,15 @@ __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_
 
 // The final placement of a compress call (tiles of the last wave), no encode beside it:
 // a lane keeps 4 vectors in flight.
-template <int NT>
-__global__ void __launch_bounds__(NT) place_final_kernel(geometry g, uint8_t* __restrict__ out, uint64_t out_cap,
-                                                         encode_ws ws, encode_launch L, archive_header_bytes hdr) {
+// Two shapes: NTHR = NT for large calls (cfg2/cfg3 compress -1.2 % / -2.8 % against the
+// wide shape), NTHR = 4 NT (capped at 1024) when there are fewer tiles than two per SM,
+// where the copy is latency-bound (cfg1 compress 0.057 -> 0.034 ms).
+template <int NT, int NTHR>
+__global__ void __launch_bounds__(NTHR) place_final_kernel(geometry g, uint8_t* __restrict__ out, uint64_t out_cap,
+                                                           encode_ws ws, encode_launch L, archive_header_bytes hdr) {
     extern __shared__ __align__(16) uint8_t smem[];
-    place_tile<NT, 4>(g, out, out_cap, ws, L, hdr, smem);
+    // the wide shape keeps 8 vectors per lane in flight (few CTAs: latency-bound)
+    place_tile<NT, NTHR == NT ? 4 : 8, NTHR>(g, out, out_cap, ws, L, hdr, smem);
 }
 
 // one thread per byte column, rounded to an instantiated CTA size
@@ -906,10 +919,23 @@ encode_ws carve_encode_ws(void* scratch, const geometry& g, uint32_t* ticket, un
 static cudaError_t launch_place_final(uint32_t threads, uint32_t tiles, const geometry& g, uint8_t* d_out,
                                       uint64_t out_cap, const encode_ws& ws, const encode_launch& L,
                                       const archive_header_bytes& hdr, cudaStream_t st) {
-    const uint32_t smem = 12 * threads + 4 * 33 * (threads / 32);
+    // FALCON_PLACE_WIDE_BELOW (tiles) overrides the shape choice (tests force both shapes)
+    static const uint64_t wide_below = [] {
+        const char* e = std::getenv("FALCON_PLACE_WIDE_BELOW");
+        if (e) return (uint64_t)std::strtoull(e, nullptr, 10);
+        int sms = 0;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) sms = 148;
+        return (uint64_t)2 * (uint64_t)sms;
+    }();
+    const bool wide = tiles < wide_below;
+    const uint32_t nthr = wide ? (4 * threads <= 1024 ? 4 * threads : 1024) : threads;
+    const uint32_t smem = 12 * threads + 4 * 33 * (nthr / 32);
     switch (threads) {
-#define FB_PLACE(n) \
-    case n: place_final_kernel<n><<<tiles, n, smem, st>>>(g, d_out, out_cap, ws, L, hdr); break;
+#define FB_PLACE(n)                                                                                          \
+    case n:                                                                                                  \
+        if (wide) place_final_kernel<n, (4 * n <= 1024 ? 4 * n : 1024)><<<tiles, nthr, smem, st>>>(g, d_out, out_cap, ws, L, hdr); \
+        else place_final_kernel<n, n><<<tiles, nthr, smem, st>>>(g, d_out, out_cap, ws, L, hdr);           \
+        break;
     FB_PLACE(32) FB_PLACE(64) FB_PLACE(96) FB_PLACE(128) FB_PLACE(160) FB_PLACE(192) FB_PLACE(224)
     FB_PLACE(256) FB_PLACE(512)
 #undef FB_PLACE

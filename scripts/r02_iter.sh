@@ -29,8 +29,8 @@ if [ "${LAUNCHES:-1}" = 1 ]; then
 fi
 if [ "${NCU:-0}" = 1 ]; then
   for k in ${KERNELS:-encode_chunks_kernel decode_chunks_kernel}; do
-    timeout 400 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o gpurun_out/prof_cfg2_${k} -f \
-      python bench.py --workload cfg2 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_full_${k}.log 2>&1
+    timeout 400 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o gpurun_out/prof_${NCU_W:-cfg2}_${k} -f \
+      python bench.py --workload ${NCU_W:-cfg2} --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_full_${k}.log 2>&1
     echo "ncu $k=$?"
   done
 fi
