@@ -143,9 +143,10 @@ __device__ void walk_frames(const uint8_t* __restrict__ arc, uint64_t len, const
                 atomicMin(ws.abort_at, (unsigned long long)b);
             } else {
                 // the block's offset stores are ordered before this point by the barrier
-                // after the write loop; one fence + release publishes them (the usual
-                // single-writer pattern: barrier, fence, flag)
-                __threadfence();
+                // after the write loop; one gpu-scope release store publishes them (barrier,
+                // then release: cumulative over what the barrier made this thread observe --
+                // CUTLASS's semaphore release).  A __threadfence() here added MEMBAR.SC +
+                // an L1 invalidate per batch.
                 st_release32(&ws.ready[b], 1u);
             }
             s_stop = code;
@@ -259,10 +260,7 @@ __device__ uint64_t walk_frames_fast(const uint8_t* __restrict__ arc, uint64_t l
             ws.chunk_size[first + i] = entry(i);
         }
         __syncthreads();
-        if (tid == 0) {  // barrier, fence, flag (see walk_frames)
-            __threadfence();
-            st_release32(&ws.ready[b], 1u);
-        }
+        if (tid == 0) st_release32(&ws.ready[b], 1u);  // barrier, release (see walk_frames)
         cursor = next;
         *cursor_out = cursor;
         if (!more) {
@@ -498,8 +496,7 @@ __device__ uint64_t walk_frames_split(const uint8_t* __restrict__ arc, uint64_t 
                 ws.chunk_size[first + i] = entry(i);
             }
             named_sync(2, kChainThreads);
-            if (wt == 0) {  // barrier, fence, flag (see walk_frames); then the slot is free
-                __threadfence();
+            if (wt == 0) {  // barrier, release (see walk_frames); then the slot is free
                 st_release32(&ws.ready[b], 1u);
                 wmbar_arrive(&s_empty[sl]);
             }

@@ -669,7 +669,7 @@ __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_
     if (valid) {
         const uint64_t b = g.batch_of(c);
         if (c == b * g.cpb) {  // first chunk of its batch: publish the batch payload prefix
-            __threadfence();
+            // (flag and value in one word: nothing else is published, no fence needed)
             st_relaxed(&ws.batch_prefix[b], (1ull << 63) | pexcl);
         }
     }
