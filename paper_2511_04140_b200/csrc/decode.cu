@@ -449,27 +449,27 @@ __device__ uint64_t walk_frames_split(const uint8_t* __restrict__ arc, uint64_t 
             const uint32_t tbr = (uint32_t)(m.cursor & 15) + 4;  // table start in the slot
             const uint32_t w0 = tbr >> 2, sh = (tbr & 3) * 8;
             auto entry = [&](uint32_t i) -> uint32_t { return __funnelshift_r(W[w0 + i], W[w0 + i + 1], sh); };
-            const uint32_t per = (exp + kChainThreads - 1) / kChainThreads;
-            const uint32_t i0 = min(exp, (uint32_t)wt * per), i1 = min(exp, i0 + per);
-            uint32_t mine = 0, big = 0;
-            for (uint32_t i = i0; i < i1; ++i) {
+            // Warp w scans entries [wb, we) (a multiple of 32 per warp) in rounds of 32
+            // consecutive entries, lane l taking entry l of the round: every smem access of the
+            // table and of s_pref is lane-contiguous.  (Thread-contiguous ranges of 16 entries
+            // put the lanes 64 B apart: 16-way bank conflicts on every read and write, which made
+            // the writer, not the chain, the walk's bound at ~6 us per batch.)
+            const uint32_t seg = ((exp + kChainThreads - 1) / kChainThreads) * 32;
+            const uint32_t wb = min(exp, (uint32_t)wwarp * seg), we = min(exp, wb + seg);
+            uint32_t wsum = 0, big = 0;
+            for (uint32_t i = wb + lane; i < we; i += 32) {
                 const uint32_t e = entry(i);
                 big |= e > emax;
-                mine += e;
+                wsum += e;
             }
-            uint32_t incl = mine;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= d) incl += t;
-            }
+            wsum = __reduce_add_sync(0xffffffffu, wsum);
             big = __reduce_or_sync(0xffffffffu, big);
-            if (lane == 31) {
-                s_wsum[wwarp] = incl;
+            if (lane == 0) {
+                s_wsum[wwarp] = wsum;
                 s_wbig[wwarp] = big;
             }
             named_sync(2, kChainThreads);
-            uint32_t run = incl - mine, anybig = 0;
+            uint32_t run = 0, anybig = 0;
 #pragma unroll
             for (int q = 0; q < kChainThreads / 32; ++q) {
                 run += q < wwarp ? s_wsum[q] : 0u;
@@ -484,9 +484,17 @@ __device__ uint64_t walk_frames_split(const uint8_t* __restrict__ arc, uint64_t 
                 }
                 break;
             }
-            for (uint32_t i = i0; i < i1; ++i) {
-                s_pref[i] = run;
-                run += entry(i);
+            for (uint32_t r0 = wb; r0 < we; r0 += 32) {
+                const uint32_t i = r0 + lane;
+                const uint32_t e = i < we ? entry(i) : 0u;
+                uint32_t incl = e;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += t;
+                }
+                if (i < we) s_pref[i] = run + incl - e;
+                run += __shfl_sync(0xffffffffu, incl, 31);
             }
             named_sync(2, kChainThreads);
             const uint64_t pay0 = m.cursor + 4 + 4 * (uint64_t)exp;
