@@ -1,8 +1,10 @@
-"""Encode launch shapes that the default sizes do not reach on small inputs, each in its own
-process (the knobs are read once per process): several encode waves with the placement of
-earlier waves fused into later launches and a wrapping image ring (FALCON_ENC_WAVE_CHUNKS),
-and both final-placement shapes (FALCON_PLACE_WIDE_BELOW: 0 = always the NT-thread shape,
-huge = always the wide one).  Every archive must equal the oracle's byte for byte."""
+"""Launch shapes that the default sizes do not reach on small inputs, each in its own process
+(the knobs are read once per process): several encode waves with the placement of earlier
+waves fused into later launches and a wrapping image ring (FALCON_ENC_WAVE_CHUNKS), both
+final-placement shapes (FALCON_PLACE_WIDE_BELOW: 0 = always the NT-thread shape, huge =
+always the wide one), and the one-role frame walker (FALCON_WALK_SERIAL, the default before
+the two-role walk).  Every archive must equal the oracle's byte for byte, every decode the
+input bit for bit."""
 import os
 import subprocess
 import sys
@@ -36,6 +38,7 @@ print("ok")
     {"FALCON_ENC_WAVE_CHUNKS": "300"},
     {"FALCON_PLACE_WIDE_BELOW": "0"},
     {"FALCON_PLACE_WIDE_BELOW": "1000000000"},
+    {"FALCON_WALK_SERIAL": "1"},
 ])
 def test_launch_shapes_match_the_oracle(env):
     r = subprocess.run([sys.executable, "-c", CHILD.format(root=ROOT)], capture_output=True, text=True,
