@@ -235,10 +235,9 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     __shared__ cert_params<T> s_cp;
     __shared__ uint32_t s_lim;   // f64 narrow-path bound for 10^A0 (used when alpha_max == A0)
     if (warp == 0) {
-#ifndef FB_P1_K
-#define FB_P1_K 4
-#endif
-        const int a = dp_alpha_k<T, FB_P1_K>(v[3]);
+        // candidate scales per step of the sampling loop (A/B, cfg2 / cfg3 compress in ms:
+        // K=2 1.289 / 1.602, K=3 1.252-1.337 / 1.598, K=4 1.251 / 1.615, K=6 1.288 / 1.614-1.707)
+        const int a = dp_alpha_k<T, sizeof(T) == 8 ? 4 : 3>(v[3]);
         const uint32_t f1 = __reduce_or_sync(0xffffffffu, a < 0 ? 0x80000000u : (1u << a));
         if (lane == 0) {
             s_flag1[0] = f1;
