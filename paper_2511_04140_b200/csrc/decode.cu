@@ -573,6 +573,11 @@ __device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
     asm volatile("" : "+r"(x));
     return x;
 }
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+    uint32_t v;
+    asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ uint32_t lds_u8_if(bool p, uint32_t a) {
     uint32_t v = 0;
     asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.u8 %0, [%1];\n\t}"
@@ -940,6 +945,7 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers, decode_min
             // compiler rebuild each load address from the shared window, 3 extra ops per load)
             const uint32_t ib = opaque_u32(smem_u32(smem)) + (uint32_t)sl * region + (uint32_t)(si.off & 15);
             const uint32_t icol = ib + (uint32_t)tid, ibm = ib + ((uint32_t)tid >> 3);
+            const uint32_t icol_s = active ? icol : ib;   // dense loads: an in-slot address for all
             const int w = (int)si.w;
             const uint32_t hA = si.hA;
             const bool case2 = hA > (uint32_t)tr::max_alpha;
@@ -965,7 +971,7 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers, decode_min
         uint32_t xb[8];
         if (dblk == 0xffu) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) xb[k] = lds_u8_if(active, icol + ro[k]);
+            for (int k = 0; k < 8; ++k) xb[k] = lds_u8(icol_s + ro[k]);   // inactive columns zeroed below
         } else {
             const uint4 wp = *reinterpret_cast<const uint4*>(&si.wpre[warp * 64 + 8 * sb]);
             const uint32_t wpre[8] = {wp.x & 0xffffu, wp.x >> 16, wp.y & 0xffffu, wp.y >> 16,
@@ -986,7 +992,7 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers, decode_min
         // byte k of x = row byte of plane 8sb+k (xb[k] <= 0xff: selector 7 reads a zero byte)
         const uint32_t xl = __byte_perm(xb[0], xb[1], 0x7740) | __byte_perm(xb[2], xb[3], 0x4077);
         const uint32_t xh = __byte_perm(xb[4], xb[5], 0x7740) | __byte_perm(xb[6], xb[7], 0x4077);
-        yb[sb] = transpose8x8(((uint64_t)xh << 32) | xl);  // byte 7-j = byte sb of lane j
+        yb[sb] = active ? transpose8x8(((uint64_t)xh << 32) | xl) : 0ull;  // byte 7-j = byte sb of lane j
     }
     // byte transpose: lane j's byte sb = byte 7-j of yb[sb]
     B z[8];

@@ -28,6 +28,7 @@
 #include "kernels.h"
 
 #include <cstdlib>
+#include <type_traits>
 
 namespace fb200 {
 
@@ -120,6 +121,9 @@ __device__ __forceinline__ uint32_t nonzero_bytes(uint32_t w) {
 // 1.39 ms at 12, 1.35 ms at 16)
 #ifndef FB_ENC_MIN_BLOCKS
 #define FB_ENC_MIN_BLOCKS 9
+#endif
+#ifndef FB_ENC_VEC_LOADS
+#define FB_ENC_VEC_LOADS 1
 #endif
 #ifndef FB_ENC_MIN_BLOCKS32
 #define FB_ENC_MIN_BLOCKS32 16
@@ -216,7 +220,47 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     {
         const T* src = in + v0 + 8u * (uint32_t)tid;
         const uint64_t pol = l2_evict_first_policy();
-        if (len == n && NC == NT) {
+        // a full chunk inside the input (not its first values before a 16-B boundary, not its
+        // last): 16-B vector loads of the window that starts at the 16-B boundary at or below
+        // value 8t (phase ph uniform per CTA: the chunk start decides it); the window ends at
+        // most 3 values past the chunk
+        const uint32_t ph = (uint32_t)(((uintptr_t)(in + v0) >> (sizeof(T) == 8 ? 3 : 2)) & (sizeof(T) == 8 ? 1u : 3u));
+        const bool vec = FB_ENC_VEC_LOADS && len == n && NC == NT && v0 >= ph && v0 + 8ull * NT + 12ull <= g.n_values;
+        if (vec) {
+            constexpr int EPV = 16 / (int)sizeof(T);             // values per vector
+            constexpr int NV = sizeof(T) == 8 ? 5 : 3;           // vectors per thread
+            T w[NV * EPV];
+            const uint4* vs = reinterpret_cast<const uint4*>(src - ph);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                const uint4 x = __ldg(vs + q);
+                if constexpr (sizeof(T) == 8) {
+                    w[2 * q] = __longlong_as_double(((long long)x.y << 32) | x.x);
+                    w[2 * q + 1] = __longlong_as_double(((long long)x.w << 32) | x.z);
+                } else {
+                    w[4 * q] = __uint_as_float(x.x);
+                    w[4 * q + 1] = __uint_as_float(x.y);
+                    w[4 * q + 2] = __uint_as_float(x.z);
+                    w[4 * q + 3] = __uint_as_float(x.w);
+                }
+            }
+            // value 8t + i is w[ph + i]; ph is uniform, so each case is straight-line code
+            auto pick = [&](auto P) {
+                constexpr int p = decltype(P)::value;
+                vprev = w[p];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[j] = w[p + 1 + j];
+            };
+            if constexpr (sizeof(T) == 8) {
+                if (ph == 0) pick(std::integral_constant<int, 0>{});
+                else pick(std::integral_constant<int, 1>{});
+            } else {
+                if (ph == 0) pick(std::integral_constant<int, 0>{});
+                else if (ph == 1) pick(std::integral_constant<int, 1>{});
+                else if (ph == 2) pick(std::integral_constant<int, 2>{});
+                else pick(std::integral_constant<int, 3>{});
+            }
+        } else if (len == n && NC == NT) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) v[j] = ld_stream(src + 1 + j, pol);
             vprev = ld_stream(src, pol);

@@ -197,3 +197,19 @@ def test_fuzz_magnitudes_at_warp_and_thread_boundaries(codec, oracle, seed):
         out.append(g.astype(np.float64) / 10.0 ** dp)
     v = np.concatenate(out)
     check(codec, oracle, v)
+
+
+@pytest.mark.parametrize("prec", [F64, F32])
+@pytest.mark.parametrize("shift", [0, 1, 2, 3])
+def test_inputs_at_every_16_byte_phase(codec, oracle, prec, shift):
+    # the encoder's 16-B vector loads start at the 16-B boundary at or below each thread's
+    # first value: inputs whose first value sits at every phase (and chunks of both parities)
+    from paper_2511_04140_b200 import synth
+    vals = synth("outlier" if prec == F64 else "mixed", 23 * N + 333, prec, seed=31 + shift, period=100)
+    base = torch.from_numpy(np.concatenate([np.zeros(shift, vals.dtype), vals])).cuda()
+    d = base[shift:]
+    assert d.data_ptr() % 16 == (shift * vals.itemsize) % 16
+    want = oracle.compress_archive(vals, N, N * 8)
+    arc, nb = codec.compress_device(d, chunk_n=N, batch_values=N * 8)
+    assert arc[:nb].cpu().numpy().tobytes() == want
+    assert torch.equal(codec.decompress_device(arc, nb).cpu(), d.cpu())
