@@ -413,33 +413,50 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
 #pragma unroll
         for (int j = 0; j < 8; ++j) o |= (uint32_t)z[j];
         orv = active ? (B)o : (B)0;
+    } else if (reuse) {
+        // (vprev is a chunk value with alpha_v <= A0, so rint is llround, as for gc)
+        B gp = (B)(S)X::to_int(X::rint_(mul_rn(vprev, scale)));
+        if (tid == 0) s_z1 = gp;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            // f64: recompute certify's integer (only wide-integer chunks get here)
+            const B gj = sizeof(B) == 8 ? (B)(S)X::to_int(X::rint_(mul_rn(v[j], scale))) : (B)(S)(int32_t)gc[j];
+            z[j] = zigzag<B>((B)(gj - gp));
+            gp = gj;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) orv |= z[j];
+        if (!active) orv = 0;
+    } else if (case2) {
+        // Case 2: the raw bit patterns, zigzagged (transform.hpp:54-55, 72-89).  Separate
+        // straight-line branches: with case2 tested inside one per-value helper the compiler
+        // kept eight copies of the predicate packed into a register on the common path.
+        B gp = zigzag<B>(X::bits(vprev));
+        if (tid == 0) s_z1 = gp;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const B gj = zigzag<B>(X::bits(v[j]));
+            z[j] = zigzag<B>((B)(gj - gp));
+            gp = gj;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) orv |= z[j];
+        if (!active) orv = 0;
     } else {
+        // Case 1 with alpha_max above the sampled A0: llround(v * 10^alpha_max)
         bool range_err = false;
         auto lane_g = [&](T x) -> B {
-            if (case2) return zigzag<B>(X::bits(x));
             const T s = mul_rn(x, scale);
             range_err |= !(fabs(s) < (T)0x1p62);  // numeric.hpp:153-154
             return (B)(S)llround_away(s);
         };
-        // (reuse: vprev is a chunk value with alpha_v <= A0, so rint is llround, as for gc)
-        B gp = reuse ? (B)(S)X::to_int(X::rint_(mul_rn(vprev, scale))) : lane_g(vprev);
+        B gp = lane_g(vprev);
         if (tid == 0) s_z1 = gp;
-        if (reuse) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                // f64: recompute certify's integer (only wide-integer chunks get here)
-                const B gj = sizeof(B) == 8 ? (B)(S)X::to_int(X::rint_(mul_rn(v[j], scale)))
-                                            : (B)(S)(int32_t)gc[j];
-                z[j] = zigzag<B>((B)(gj - gp));
-                gp = gj;
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const B gj = lane_g(v[j]);
-                z[j] = zigzag<B>((B)(gj - gp));
-                gp = gj;
-            }
+        for (int j = 0; j < 8; ++j) {
+            const B gj = lane_g(v[j]);
+            z[j] = zigzag<B>((B)(gj - gp));
+            gp = gj;
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) orv |= z[j];
