@@ -820,6 +820,7 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers, decode_min
         const bool aligned = ((uintptr_t)arc & 15) == 0;
         // dynamic chunk tickets (measured better balanced than static striding); lane 0
         // waits for the chunk's batch frame and loads its offset and size
+        uint32_t known_ready = 0;   // lane 0: batches [0, known_ready) seen published
         auto fetch = [&](uint32_t it, uint32_t& t, uint32_t& kind, uint64_t& off, uint32_t& size) {
             uint32_t tk = 0;
             if (lane == 0) tk = atomicAdd(ws.ticket, 1u);
@@ -831,12 +832,18 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers, decode_min
             size = 0;
             if (kind == SLOT_CHUNK && lane == 0) {
                 const uint32_t b = t / g.cpb;
-                while (ld_acquire32(&ws.ready[b]) == 0) {
-                    if (*(volatile unsigned long long*)ws.abort_at <= b) {
-                        kind = SLOT_SKIP;
-                        break;
+                // the walker publishes batches in order with release stores, so one acquire
+                // that saw batch b' published covers every batch <= b': no flag round trip
+                // on the ticket -> offsets chain for those
+                if (b + 1 > known_ready) {
+                    while (ld_acquire32(&ws.ready[b]) == 0) {
+                        if (*(volatile unsigned long long*)ws.abort_at <= b) {
+                            kind = SLOT_SKIP;
+                            break;
+                        }
+                        __nanosleep(64);
                     }
-                    __nanosleep(64);
+                    if (kind == SLOT_CHUNK) known_ready = b + 1;
                 }
                 if (kind == SLOT_CHUNK) {
                     off = ws.chunk_off[t];
