@@ -125,9 +125,6 @@ __device__ __forceinline__ uint32_t nonzero_bytes(uint32_t w) {
 #ifndef FB_ENC_VEC_LOADS
 #define FB_ENC_VEC_LOADS 1
 #endif
-#ifndef FB_PLACE_BULK
-#define FB_PLACE_BULK 1
-#endif
 #ifndef FB_ENC_MIN_BLOCKS32
 #define FB_ENC_MIN_BLOCKS32 16
 #endif
@@ -135,7 +132,7 @@ template <typename T, int NT>
 constexpr int encode_min_blocks() {
     return NT <= 128 ? (sizeof(T) == 4 ? FB_ENC_MIN_BLOCKS32 : FB_ENC_MIN_BLOCKS) : (2048 / NT > 0 ? 2048 / NT : 1);
 }
-template <int NT, int U, int NTHR = NT, bool BULK = false>
+template <int NT, int U, int NTHR = NT>
 __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_t out_cap, const encode_ws& ws,
                            const encode_launch& L, const archive_header_bytes& hdr, uint8_t* smem);
 
@@ -661,122 +658,7 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
 // over all NTHR / 32 warps, each moving NT * 32 / NTHR chunks (the final placement runs with
 // more threads than chunks: with 32 chunks per warp a small input was a chain of dependent
 // round trips per lane).
-// Final placement's copy through shared memory: each warp stages its chunks' images with
-// one bulk (TMA-engine) copy per chunk into a 16 KB byte ring (up to kBulkSlots chunks in
-// flight, mbarrier completion), then writes them out funnel-shifted from smem.  The
-// register-staged copy keeps at most U 16-B vectors per lane in flight (64 KB per SM at
-// 8 resident CTAs); the ring keeps up to 16 KB per warp in flight without registers.
-constexpr uint32_t kBulkRing = 16384;
-constexpr int kBulkSlots = 8;
-__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-template <int NT, int CPW>
-__device__ void place_copy_bulk(const geometry& g, uint8_t* __restrict__ out, uint64_t out_cap, const encode_ws& ws,
-                                const encode_launch& L, uint64_t t, const uint64_t* s_off, const uint32_t* s_sz,
-                                uint8_t* ring, uint64_t* bars, uint32_t* rpos, int warp, int lane) {
-    const int c0 = warp * CPW;   // first chunk of this warp in the tile
-    int nch = 0;                 // chunks of this warp that exist
-    for (int k = 0; k < CPW; ++k) nch += (t * NT + (uint64_t)(c0 + k) < g.n_chunks) ? 1 : 0;
-    if (lane == 0) {
-        for (int i = 0; i < kBulkSlots; ++i)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&bars[i])), "r"(1u) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    auto image = [&](int k) -> const uint8_t* {
-        const uint64_t cc = t * NT + (uint64_t)(c0 + k);
-        uint32_t rs = L.place_slot0 + (uint32_t)(cc - L.place_c0);   // = cc mod ring
-        rs = rs >= ws.ring ? rs - (uint32_t)ws.ring : rs;
-        return ws.images + rs * (uint64_t)ws.slot;
-    };
-    // bytes staged for chunk k: the image plus the 4 readable bytes the funnel loads touch;
-    // 0 for a chunk that does not fit the output (its capacity error is recorded below)
-    auto nbytes = [&](int k) -> uint32_t {
-        const uint64_t off = s_off[c0 + k];
-        const uint32_t size = s_sz[c0 + k];
-        return off + size > out_cap ? 0u : (size + 4 + 15) & ~15u;
-    };
-    uint32_t head = 0, tail = 0;   // ring byte counters (positions = counter mod kBulkRing)
-    uint32_t* rend = rpos + kBulkSlots;   // [slot]: allocation end (counter) of the staged chunk
-    int k_issue = 0;
-    for (int k = 0; k < nch; ++k) {
-        // stage every chunk that fits the ring and the slots (all lanes compute the same
-        // allocation; lane 0 issues)
-        while (k_issue < nch && k_issue - k < kBulkSlots) {
-            const uint32_t nb = nbytes(k_issue);
-            uint32_t pos = head % kBulkRing;
-            uint32_t h2 = head;
-            if (pos + nb > kBulkRing) {   // no wrap inside a chunk: skip to the ring start
-                h2 += kBulkRing - pos;
-                pos = 0;
-            }
-            if (k_issue == k) tail = h2;   // nothing in flight: the whole ring is free
-            if (h2 + nb - tail > kBulkRing) break;   // wait for older chunks to drain
-            if (lane == 0) {
-                rpos[k_issue % kBulkSlots] = pos;
-                rend[k_issue % kBulkSlots] = h2 + nb;
-                const uint32_t bar = smem_addr(&bars[k_issue % kBulkSlots]);
-                if (nb) {
-                    // the ring bytes were last read by generic loads of an older chunk
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(nb) : "memory");
-                    asm volatile(
-                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                            smem_addr(ring + pos)),
-                        "l"(image(k_issue)), "r"(nb), "r"(bar)
-                        : "memory");
-                } else {
-                    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(bar) : "memory");
-                }
-            }
-            head = h2 + nb;
-            ++k_issue;
-        }
-        __syncwarp();
-        // chunk k: wait for its bytes, write it out funnel-shifted
-        {
-            uint32_t done = 0;
-            const uint32_t bar = smem_addr(&bars[k % kBulkSlots]);
-            const uint32_t par = (uint32_t)(k / kBulkSlots) & 1u;
-            while (!done) {
-                asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-                             : "=r"(done) : "r"(bar), "r"(par) : "memory");
-            }
-        }
-        const uint32_t nb = nbytes(k);
-        const uint64_t off = s_off[c0 + k];
-        const uint32_t size = s_sz[c0 + k];
-        if (nb == 0) {
-            if (lane == 0) record_error(ws.error, t * NT + (uint64_t)(c0 + k), DEV_E_CAPACITY);
-        } else {
-            const uint8_t* img = ring + rpos[k % kBulkSlots];
-            const uint32_t a = (uint32_t)(off & 15);
-            const uint32_t end = a + size;
-            const uint32_t nv = (end + 15) >> 4;
-            for (uint32_t vv = lane; vv < nv; vv += 32) {
-                const uint32_t lo = vv << 4, hi = lo + 16;
-                uint8_t* dst = out + (off - a) + lo;
-                if (lo >= a && hi <= end) {
-                    const uint32_t sb = lo - a;
-                    const uint32_t* w = reinterpret_cast<const uint32_t*>(img) + (sb >> 2);
-                    const uint32_t sh = (sb & 3) * 8;
-                    uint32_t r[5];
-#pragma unroll
-                    for (int i = 0; i < 5; ++i) r[i] = w[i];
-                    *reinterpret_cast<uint4*>(dst) =
-                        make_uint4(__funnelshift_r(r[0], r[1], sh), __funnelshift_r(r[1], r[2], sh),
-                                   __funnelshift_r(r[2], r[3], sh), __funnelshift_r(r[3], r[4], sh));
-                } else {
-                    const uint32_t from = lo > a ? lo : a, to = hi < end ? hi : end;
-                    for (uint32_t i = from; i < to; ++i) out[(off - a) + i] = img[i - a];
-                }
-            }
-        }
-        __syncwarp();   // every lane's reads of chunk k are done before its bytes are reused
-        tail = rend[k % kBulkSlots];
-    }
-}
-
-template <int NT, int U, int NTHR, bool BULK>
+template <int NT, int U, int NTHR>
 __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_t out_cap, const encode_ws& ws,
                            const encode_launch& L, const archive_header_bytes& hdr, uint8_t* smem) {
     constexpr int kPlaceTile = NT;
@@ -890,14 +772,6 @@ __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_
         for (int i = 0; i < 47; ++i) out[i] = hdr.b[i];
     }
 
-    if constexpr (BULK) {
-        // (no FB_L2_HINTS discard here: a final placement's images are read once)
-        __shared__ __align__(8) uint64_t s_bars[NCW][kBulkSlots];
-        __shared__ uint32_t s_rpos[NCW][2 * kBulkSlots];
-        uint8_t* ring = smem + ((12 * NT + 4 * 33 * NCW + 127) & ~127) + (size_t)warp * kBulkRing;
-        place_copy_bulk<NT, CPW>(g, out, out_cap, ws, L, t, s_off, s_sz, ring, s_bars[warp], s_rpos[warp], warp, lane);
-        return;
-    }
     // copy: each warp moves its CPW chunks as one flat list of destination vectors, so a
     // lane's consecutive vectors are independent (their loads overlap) instead of the
     // chunks being copied one after another
@@ -999,10 +873,8 @@ template <int NT, int NTHR>
 __global__ void __launch_bounds__(NTHR) place_final_kernel(geometry g, uint8_t* __restrict__ out, uint64_t out_cap,
                                                            encode_ws ws, encode_launch L, archive_header_bytes hdr) {
     extern __shared__ __align__(16) uint8_t smem[];
-    // the wide shape keeps 8 vectors per lane in flight (few CTAs: latency-bound); the
-    // NT-thread shape stages the images through smem with bulk copies (place_copy_bulk)
-    // (chunk images up to 8.2 KB, i.e. NT <= 128, fit a 16 KB ring)
-    place_tile<NT, NTHR == NT ? 4 : 8, NTHR, NTHR == NT && NT <= 128 && FB_PLACE_BULK>(g, out, out_cap, ws, L, hdr, smem);
+    // the wide shape keeps 8 vectors per lane in flight (few CTAs: latency-bound)
+    place_tile<NT, NTHR == NT ? 4 : 8, NTHR>(g, out, out_cap, ws, L, hdr, smem);
 }
 
 // one thread per byte column, rounded to an instantiated CTA size
@@ -1120,19 +992,12 @@ static cudaError_t launch_place_final(uint32_t threads, uint32_t tiles, const ge
     }();
     const bool wide = tiles < wide_below;
     const uint32_t nthr = wide ? (4 * threads <= 1024 ? 4 * threads : 1024) : threads;
-    uint32_t smem = 12 * threads + 4 * 33 * (nthr / 32);
-    const bool bulk = !wide && FB_PLACE_BULK && threads <= 128;
-    if (bulk) smem = ((smem + 127) & ~127u) + (threads / 32) * kBulkRing;   // staging rings
-    cudaError_t e;
+    const uint32_t smem = 12 * threads + 4 * 33 * (nthr / 32);
     switch (threads) {
 #define FB_PLACE(n)                                                                                          \
     case n:                                                                                                  \
-        if (wide) {                                                                                          \
-            place_final_kernel<n, (4 * n <= 1024 ? 4 * n : 1024)><<<tiles, nthr, smem, st>>>(g, d_out, out_cap, ws, L, hdr); \
-        } else {                                                                                             \
-            if ((e = ensure_dynamic_smem((const void*)place_final_kernel<n, n>, smem))) return e;          \
-            place_final_kernel<n, n><<<tiles, nthr, smem, st>>>(g, d_out, out_cap, ws, L, hdr);             \
-        }                                                                                                    \
+        if (wide) place_final_kernel<n, (4 * n <= 1024 ? 4 * n : 1024)><<<tiles, nthr, smem, st>>>(g, d_out, out_cap, ws, L, hdr); \
+        else place_final_kernel<n, n><<<tiles, nthr, smem, st>>>(g, d_out, out_cap, ws, L, hdr);           \
         break;
     FB_PLACE(32) FB_PLACE(64) FB_PLACE(96) FB_PLACE(128) FB_PLACE(160) FB_PLACE(192) FB_PLACE(224)
     FB_PLACE(256) FB_PLACE(512)
