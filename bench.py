@@ -565,6 +565,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: FALCON_BENCH_ONE_GPU=1 puts every rank on GPU 0 and exchanges over gloo, so
+    # the multi-rank path (shards, exchange, max-over-ranks timing) runs on a one-GPU box
+    one_gpu = os.environ.get("FALCON_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local_rank = 0
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -572,7 +577,10 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:
