@@ -831,7 +831,7 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers, decode_min
             off = 0;
             size = 0;
             if (kind == SLOT_CHUNK && lane == 0) {
-                const uint32_t b = t / g.cpb;
+                const uint32_t b = (uint32_t)g.batch_of(t);
                 // the walker publishes batches in order with release stores, so one acquire
                 // that saw batch b' published covers every batch <= b': no flag round trip
                 // on the ticket -> offsets chain for those
@@ -898,7 +898,7 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers, decode_min
                 si.size = size;
                 if (kind == SLOT_CHUNK) {
                     // chunk-uniform values the consumers would otherwise each recompute
-                    const uint32_t b = t / g.cpb;
+                    const uint32_t b = (uint32_t)g.batch_of(t);
                     const uint32_t ci = t - b * g.cpb;
                     const uint64_t left = g.values_in(b) - (uint64_t)ci * n;
                     si.v0 = (uint64_t)b * g.batch_values + (uint64_t)ci * n;

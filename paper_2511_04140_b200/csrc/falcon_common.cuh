@@ -240,8 +240,17 @@ struct geometry {
     uint64_t n_batches;
     uint64_t n_chunks;       // total chunks over all batches
     uint32_t last_cpb;       // chunks in the final batch
+    uint64_t cpb_magic;      // ceil(2^64 / cpb) (0 when cpb == 1), make_geometry
 
-    __host__ __device__ uint64_t batch_of(uint64_t c) const { return c / cpb; }
+    // c / cpb; on the device one 64-bit multiply-high (exact for c < 2^32 chunks: the error
+    // of ceil(2^64/cpb) moves c/cpb by less than 2^-32 < 1/cpb)
+    __host__ __device__ uint64_t batch_of(uint64_t c) const {
+#ifdef __CUDA_ARCH__
+        return cpb_magic ? __umul64hi(c, cpb_magic) : c;
+#else
+        return c / cpb;
+#endif
+    }
     __host__ __device__ uint32_t chunks_in(uint64_t b) const {
         return b + 1 == n_batches ? last_cpb : cpb;
     }

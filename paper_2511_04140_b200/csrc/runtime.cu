@@ -78,6 +78,7 @@ falcon_status make_geometry(uint64_t n, uint32_t chunk_n, uint64_t bv, uint64_t 
     g.chunk_n = chunk_n;
     const uint64_t cpb = (bv + chunk_n - 1) / chunk_n;
     g.n_batches = n ? (n + bv - 1) / bv : 0;
+    g.cpb_magic = 0;
     if (g.n_batches == 0) {
         g.cpb = 1;
         g.last_cpb = 0;
@@ -90,6 +91,7 @@ falcon_status make_geometry(uint64_t n, uint32_t chunk_n, uint64_t bv, uint64_t 
         return set_error(FALCON_ERR_INVALID, "append_batch: too many chunks");  // container.cpp:90-91
     g.cpb = g.n_batches > 1 ? (uint32_t)cpb : g.last_cpb;
     g.n_chunks = (g.n_batches - 1) * (uint64_t)g.cpb + g.last_cpb;
+    g.cpb_magic = g.cpb > 1 ? ~0ull / g.cpb + 1 : 0;
     if (g.n_chunks + 1 > 0x7fffffffull)
         return set_error(FALCON_ERR_UNSUPPORTED,
                          "more than 2^31-2 chunks in one device call; shard the input");
