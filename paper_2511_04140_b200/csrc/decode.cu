@@ -1,10 +1,12 @@
-// decode.cu -- single-launch Falcon decompress for sm_100a (persistent, warp-specialised).
+// decode.cu -- Falcon decompress for sm_100a: frame walker + persistent, warp-specialised
+// decoder, launched back to back with programmatic dependent launch.
 //
 // The archive has no batch index (FORMAT.md:10-14): batch b+1's frame starts where
-// batch b's payload ends, so frames must be located sequentially.  Block 0 of the launch
-// is the *frame walker* (read_batch chain, container.cpp:113-132, pipeline.hpp:394-417):
-// per batch it loads the size table with vector loads, validates the frame, scans it
-// into per-chunk offsets and publishes the batch.  In every other block:
+// batch b's payload ends, so frames must be located sequentially.  walker_kernel (one
+// block) is the *frame walker* (read_batch chain, container.cpp:113-132,
+// pipeline.hpp:394-417): per batch its chain warps load the count + size table with 16-B
+// vector loads and sum it, its writer warps validate the entries, scan them into per-chunk
+// offsets and publish the batch (walk_frames_split).  In every decoder block:
 //   producers (2 warps)  take chunk tickets, wait for the chunk's batch, stage the chunk
 //                        bytes into a smem slot ring (cp.async at the 16-B phase), and
 //                        parse + validate it in the reference's check order

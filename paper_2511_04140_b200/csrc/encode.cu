@@ -1,11 +1,13 @@
-// encode.cu -- Falcon compress for sm_100a: encode_chunks_kernel + place_chunks_kernel.
+// encode.cu -- Falcon compress for sm_100a: encode_chunks_kernel + place_final_kernel.
 //
 // encode_chunks_kernel: one CTA per chunk (chunk_n values: z1 + (chunk_n-1) delta
 // lanes).  Thread t owns the "byte column" t: delta lanes 8t..8t+7 (values 8t+1..8t+8),
 // which is exactly byte t of every bit-plane row (FORMAT.md:79-84), so planes come out of
 // per-thread 8x8 bit transposes.
 //
-//   load     each thread loads its 8 values + the preceding one into registers
+//   load     each thread loads its 8 values + the preceding one into registers (16-B
+//            vector loads of its window; the chunk one CTA generation ahead is pulled
+//            into L2 with a bulk prefetch)
 //   analyze  phase 1: warp 0 runs the exact dp_ds loop on 32 samples -> A0 (attained)
 //            phase 2: every value gets the one-sided lean certification at A0
 //            (dpds.cuh); the few it cannot decide run the exact loop.  alpha_max,
@@ -20,9 +22,10 @@
 //            rows: bitmap bytes + payload at warp prefix + ballot rank,
 //            bitplane.hpp:126-148); 16-B stores into the chunk's scratch slot
 //
-// place_chunks_kernel: scan of the chunk sizes in tiles with a decoupled look-back, then
-// the images are copied to their archive offsets and the batch tables and the header
-// are written (container.cpp:44-55, 88-111).
+// placement (place_tile: grid row 0 of a later wave's encode launch, and
+// place_final_kernel after the last wave): scan of the chunk sizes in tiles with a
+// decoupled look-back, then the images are copied to their archive offsets and the batch
+// tables and the header are written (container.cpp:44-55, 88-111).
 #include "dpds.cuh"
 #include "falcon_common.cuh"
 #include "kernels.h"
