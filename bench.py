@@ -232,8 +232,9 @@ def link_bandwidth(torch, dev, host_pinned):
 
 
 def our_launches_per_step(n_values, prec):
-    """Kernels of one compress + decompress (csrc/encode.cu plan_waves, decode.cu): one
-    encode launch per wave of batches + the final placement, then walker + decoder."""
+    """Kernels of one compress + decompress (csrc/encode.cu plan_waves, decode.cu): the
+    chunk sampler, one encode launch per wave of batches + the final placement, then
+    walker + decoder."""
     if n_values == 0:
         return 0
     nb = (n_values + BATCH_VALUES - 1) // BATCH_VALUES
@@ -244,7 +245,7 @@ def our_launches_per_step(n_values, prec):
     wave = int(os.environ.get("FALCON_ENC_WAVE_CHUNKS", "0")) or (n_chunks if slots >= n_chunks
                                                                    else (slots - 128) // 2)
     wb = nb if wave >= n_chunks else max(1, min(wave // cpb, 65534, nb))
-    return (nb + wb - 1) // wb + 1 + 2
+    return 1 + (nb + wb - 1) // wb + 1 + 2
 
 
 def run_ours(args, rank, world, local_rank):

@@ -2,7 +2,10 @@
 // (dp_ds_calculate_counted, reference numeric.hpp:108-140).  Included only by the
 // kernel translation unit.  Every function returns exactly what the reference loop
 // decides; DESIGN.md "Exact fast analysis" carries the proofs, and
-// tests/test_gpu_dpds.py checks them against the CPU oracle on 10^8 inputs.
+// tests/test_gpu_dpds.py checks them against the CPU oracle on ~1.6 M adversarial f64
+// inputs (random bit patterns, decimals, 1-3 ulp perturbations, decade edges) per candidate
+// scale (10 scales), ~1.2 M f32 inputs per scale (7 scales); the full-size parity gates
+// cover the encoder's use of them on every config's whole archive.
 //
 // (1) Gap test.  The reference accepts scale a when |s - round(s)| <= |s| * 2^-52 with
 //     s = RN(v * 10^a).  Writing s = M * 2^(E-52) (M in [2^52, 2^53)) and G for the
@@ -186,8 +189,8 @@ __device__ __forceinline__ float div_pow10_markstein(float g, float p, float rp)
 
 enum : int { CERT_UNDECIDED = 0, CERT_OK = 1, CERT_EXC = 2 };
 
-// Branch-free form of dp_certify for the encoder's hot loop: same verdicts (the
-// self-test compares the two), written with selects so the unrolled per-thread
+// SELF-TEST ONLY (selftest.cu; the encoder uses certify_lean below): branch-free form of
+// dp_certify with the same verdicts (the self-test compares the two), written with selects so the unrolled per-thread
 // values interleave.  Also returns floor_log10(|v|) of nonzero normal values
 // (max over the chunk gives floor_log10(max|v|) for beta_hat, transform.hpp:62-63);
 // *mag = INT_MIN for zeros and specials.
@@ -336,7 +339,8 @@ __device__ __forceinline__ bool certify_lean(float v, const cert_params<float>& 
     return inr && notpow2 && fabsf(e) < H;
 }
 
-// (3): decide v against candidate scale A (0 <= A <= max_alpha).  CERT_OK: alpha_v <= A
+// SELF-TEST ONLY (selftest.cu, the specification certify_lean / certify_fast are checked
+// against).  (3): decide v against candidate scale A (0 <= A <= max_alpha).  CERT_OK: alpha_v <= A
 // and v is not an exception, *g = round_half_away(v*10^A).  CERT_EXC: v is an
 // exception.  CERT_UNDECIDED: run dp_alpha_full.
 template <typename T>

@@ -8,7 +8,8 @@
 //   load     each thread loads its 8 values + the preceding one into registers (16-B
 //            vector loads of its window; the chunk one CTA generation ahead is pulled
 //            into L2 with a bulk prefetch)
-//   analyze  phase 1: warp 0 runs the exact dp_ds loop on 32 samples -> A0 (attained)
+//   analyze  phase 1 (sample_chunks_kernel, ahead of the encode launch): the exact dp_ds
+//            loop on 32 samples of the chunk -> A0 (attained)
 //            phase 2: every value gets the one-sided lean certification at A0
 //            (dpds.cuh); the few it cannot decide run the exact loop.  alpha_max,
 //            exceptions, max|v| (numeric.hpp:108-140, transform.hpp:47-68), bit-exact
@@ -40,6 +41,29 @@ namespace {
 constexpr uint64_t kFlagAgg = 1ull << 62;
 constexpr uint64_t kFlagInc = 2ull << 62;
 constexpr uint64_t kValMask = (1ull << 62) - 1;
+
+// chunk-uniform certification parameters at scale A (constant table, tables.cu)
+__device__ __forceinline__ cert_params<double> cert_params_at(double, int A) {
+    const cert_row64& r = g_cert_f64[A];
+    cert_params<double> c;
+    c.p = r.p;
+    c.lo1 = r.lo1;
+    c.span = r.span;
+    c.hk = r.hk;
+    c.plo = r.plo;
+    return c;
+}
+__device__ __forceinline__ cert_params<float> cert_params_at(float, int A) {
+    const cert_row32& r = g_cert_f32[A];
+    cert_params<float> c;
+    c.p = r.p;
+    c.lo = r.lo;
+    c.span = r.span;
+    c.hk = r.hk;
+    return c;
+}
+__device__ __forceinline__ uint32_t narrow_lim(double, int A) { return g_cert_f64[A].lim; }
+__device__ __forceinline__ uint32_t narrow_lim(float, int) { return 0u; }
 
 template <typename B>
 __device__ __forceinline__ B warp_or(B v);
@@ -135,6 +159,40 @@ template <typename T, int NT>
 constexpr int encode_min_blocks() {
     return NT <= 128 ? (sizeof(T) == 4 ? FB_ENC_MIN_BLOCKS32 : FB_ENC_MIN_BLOCKS) : (2048 / NT > 0 ? 2048 / NT : 1);
 }
+// Phase 1 of every chunk ahead of the encode launch: kSamples lanes per chunk sample the
+// chunk's first values, run the exact dp_ds loop on them (numeric.hpp:108-140) and store
+// the OR of the one-hot alphas (bit 31: an exception).  The encoder then certifies at
+// A0 = the largest sampled alpha with no warp-0-only phase and no barrier before phase 2
+// (that phase was the encoder's top stall: 19 % of its stall samples on cfg2).  A0 only
+// selects the encoder's fast path (alpha_max == A0), never the output.  The exact loop is
+// ~250 warp-instructions per sample step, so the sampler is issue-bound: 8 samples per
+// chunk (4 chunks per warp) instead of the 32 of the in-kernel phase it replaces (cfg2
+// sampler 78 us at 32 samples per chunk).
+constexpr int kSamples = 8;
+template <typename T>
+__global__ void __launch_bounds__(256) sample_chunks_kernel(const T* __restrict__ in, geometry g,
+                                                            uint32_t* __restrict__ look) {
+    constexpr int CPW = 32 / kSamples;   // chunks per warp
+    const int lane = threadIdx.x & 31;
+    const uint64_t c = ((uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * CPW + (uint64_t)(lane / kSamples);
+    const uint32_t n = g.chunk_n;
+    const uint32_t i = (uint32_t)(lane % kSamples) % n;
+    T v = T(0);
+    if (c < g.n_chunks) {
+        const uint64_t b = g.batch_of(c);
+        const uint64_t ci = c - b * g.cpb;
+        const uint64_t left = g.values_in(b) - ci * n;
+        const uint32_t len = left < n ? (uint32_t)left : n;
+        // values past a short final chunk are its +0.0 padding (pipeline.hpp:205-215)
+        if (i < len) v = __ldg(in + b * g.batch_values + ci * n + i);
+    }
+    const int a = dp_alpha_k<T, sizeof(T) == 8 ? 4 : 3>(v);
+    uint32_t f = a < 0 ? 0x80000000u : (1u << a);
+#pragma unroll
+    for (int d = 1; d < kSamples; d <<= 1) f |= __shfl_xor_sync(0xffffffffu, f, d);
+    if (lane % kSamples == 0 && c < g.n_chunks) look[c] = f;
+}
+
 template <int NT, int U, int NTHR = NT>
 __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_t out_cap, const encode_ws& ws,
                            const encode_launch& L, const archive_header_bytes& hdr, uint8_t* smem);
@@ -161,7 +219,7 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     // [block][thread] u64: byte k of entry (s, t) = row byte t of bit plane 8s+k
     uint64_t* s_planes = reinterpret_cast<uint64_t*>(smem + encode_stage_bytes<T>(n));
 
-    __shared__ uint32_t s_flag1[nwarps], s_flag2[nwarps];  // bit 31 exception | one-hot alphas
+    __shared__ uint32_t s_flag2[nwarps];                   // bit 31 exception | one-hot alphas
     __shared__ uint32_t s_mag[nwarps];                     // max floor_log10 + 1024 (0: none)
     __shared__ uint32_t s_warpw[nwarps];
     __shared__ __align__(16) uint32_t s_rowoff[64];        // plane p: row offset in the image
@@ -193,6 +251,10 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     const uint32_t c = b * g.cpb + ci;                      // < 2^31 chunks per launch
     const uint64_t v0 = (uint64_t)b * g.batch_values + (uint64_t)ci * n;
     const bool active = tid < NC;
+
+    // ---- phase 1 (sample_chunks_kernel): this chunk's sample verdict, loaded beside the
+    //      values (f32: after them -- the 32-register budget spilled with it early) ----
+    uint32_t F = sizeof(T) == 8 ? __ldg(ws.look + c) : 0u;
 
     // The chunk L.pf_ahead CTAs later (about one generation of resident CTAs) is pulled into
     // L2 with one bulk prefetch, so its CTA's value loads hit L2 instead of waiting on DRAM
@@ -275,26 +337,10 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
         }
     }
 
-    // ---- analyze, phase 1: warp 0 runs the exact loop on 32 samples of its own values
-    //      (value 8L + 4 of lane L: no extra load on the critical path) -> A0 = the
-    //      largest sampled alpha (attained, so alpha_max >= A0); lane 0 also prepares
-    //      the chunk-uniform certification parameters for everybody ----
-    __shared__ cert_params<T> s_cp;
-    __shared__ uint32_t s_lim;   // f64 narrow-path bound for 10^A0 (used when alpha_max == A0)
-    if (warp == 0) {
-        // candidate scales per step of the sampling loop (A/B, cfg2 / cfg3 compress in ms:
-        // K=2 1.289 / 1.602, K=3 1.252-1.337 / 1.598, K=4 1.251 / 1.615, K=6 1.288 / 1.614-1.707)
-        const int a = dp_alpha_k<T, sizeof(T) == 8 ? 4 : 3>(v[3]);
-        const uint32_t f1 = __reduce_or_sync(0xffffffffu, a < 0 ? 0x80000000u : (1u << a));
-        if (lane == 0) {
-            s_flag1[0] = f1;
-            const int a0 = (f1 & 0x7fffffffu) ? 31 - __clz((int)(f1 & 0x7fffffffu)) : 0;
-            s_cp = cert_params_for(T{}, a0);
-            s_lim = (2074u - ((uint32_t)__double2hiint((double)X::pow10(a0)) >> 20)) << 20;
-        }
-    }
-    __syncthreads();
-    uint32_t F = s_flag1[0];
+    // ---- analyze, phase 1 (decided ahead by sample_chunks_kernel): A0 = the largest
+    //      alpha of 32 sampled chunk values, attained, so alpha_max >= A0; bit 31 = a
+    //      sampled exception (the chunk is Case 2, phase 2 is skipped) ----
+    if (sizeof(T) == 4) F = __ldg(ws.look + c);
     const int A0 = (F & 0x7fffffffu) ? 31 - __clz((int)(F & 0x7fffffffu)) : 0;
 
     // ---- analyze, phase 2: lean certification of every value at A0 (dpds.cuh); the
@@ -307,7 +353,7 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     uint32_t f2 = 0;     // exception bit | one-hot alphas of values decided by the exact loop
     uint32_t mx = 0;     // max |v| high word (f32: bits) -> floor_log10(max|v|) for beta_hat
     if (active && !(F >> 31)) {
-        const cert_params<T> cp = s_cp;
+        const cert_params<T> cp = cert_params_at(T{}, A0);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             uint32_t ah;
@@ -334,7 +380,7 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
             if (a < 0) break;  // the chunk is Case 2: nothing else matters
         }
     }
-    f2 = __reduce_or_sync(0xffffffffu, f2);
+    f2 = __reduce_or_sync(0xffffffffu, f2) | F;   // + the sample's flags
     const uint32_t mxw = __reduce_max_sync(0xffffffffu, mx);
     if (lane == 0) {
         s_flag2[warp] = f2;
@@ -398,8 +444,8 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     // would miss a wide value there (transform.hpp:87-88 wraps in 64 bits).
     const T scale = X::pow10(case2 ? 0 : amax);
     const bool reuse = !case2 && amax == A0;
-    // (reuse: scale = 10^A0, whose bound phase 1 computed)
-    const bool narrow = sizeof(B) == 8 && reuse && M < s_lim;
+    // (reuse: scale = 10^A0, whose 32-bit bound is in the table)
+    const bool narrow = sizeof(B) == 8 && reuse && M < narrow_lim(T{}, A0);
     B z[8];
     B orv = 0;
     if (narrow) {
@@ -954,6 +1000,7 @@ size_t encode_scratch_bytes(const geometry& g) {
     b += (g.n_chunks * 4 + 15) & ~15ull;                 // sizes
     b += w.tiles * 8;                                     // tile status
     b += (g.n_batches + 1) * 8;                           // batch prefixes
+    b += g.n_chunks * 4;                                  // sample verdicts (phase 1)
     b = (b + 255) & ~255ull;
     b += w.ring * (uint64_t)encode_slot_bytes<T>(g.chunk_n);  // image ring
     return b;
@@ -971,6 +1018,8 @@ encode_ws carve_encode_ws(void* scratch, const geometry& g, uint32_t* ticket, un
     p += w.tiles * 8;
     ws.batch_prefix = reinterpret_cast<uint64_t*>(p);
     p += (g.n_batches + 1) * 8;
+    ws.look = reinterpret_cast<uint32_t*>(p);
+    p += g.n_chunks * 4;
     const size_t used = (size_t)(p - static_cast<uint8_t*>(scratch));
     p = static_cast<uint8_t*>(scratch) + ((used + 255) & ~255ull);
     ws.images = p;
@@ -1022,7 +1071,8 @@ cudaError_t launch_encode(const T* d_in, const geometry& g, uint8_t* d_out, uint
         return g.header_bytes ? cudaMemcpyAsync(d_out, hdr.b, 47, cudaMemcpyHostToDevice, st) : cudaSuccess;
     }
     const wave_plan w = plan_waves(g, encode_slot_bytes<T>(g.chunk_n));
-    // tile status + batch prefixes are contiguous
+    // tile status + batch prefixes are contiguous (sample_chunks_kernel writes every
+    // chunk's sample verdict)
     if ((e = cudaMemsetAsync(ws.tile_status, 0, (w.tiles + g.n_batches + 1) * 8, st))) return e;
     if ((e = cudaMemsetAsync(ws.ticket, 0, sizeof(uint32_t), st))) return e;
     const uint32_t threads = encode_block_threads(g.chunk_n);
@@ -1044,6 +1094,11 @@ cudaError_t launch_encode(const T* d_in, const geometry& g, uint8_t* d_out, uint
     if (!kern) return cudaErrorInvalidConfiguration;
     if ((e = ensure_dynamic_smem((const void*)kern, smem))) return e;
     if (ev0 && (e = cudaEventRecord(ev0, st))) return e;
+    {   // phase 1 of every chunk (its sample verdict) ahead of the encode launches
+        const uint64_t per_block = 8 * (32 / kSamples);
+        sample_chunks_kernel<T><<<(unsigned)((g.n_chunks + per_block - 1) / per_block), 256, 0, st>>>(d_in, g, ws.look);
+        if ((e = cudaGetLastError())) return e;
+    }
     uint64_t placed = 0;
     for (uint64_t k = 0; k <= w.launches; ++k) {
         encode_launch L;

@@ -71,6 +71,29 @@ FB_TABLE_SPACE uint64_t g_decade_f64[618];  // + guard entry (+inf) for exponent
 FB_TABLE_SPACE uint32_t g_decade_f32[78];   // + guard entry (+inf) for exponent 0xff
 #endif
 
+// The encoder's chunk-uniform certification parameters per candidate scale A (dpds.cuh
+// cert_params, built on the host from the tables above by upload_tables): one uniform
+// constant-bank read instead of a dependent table chain after the chunk's A0 is known.
+struct cert_row64 {
+    double p;          // 10^A
+    uint32_t lo1;      // hi(dec(-A)) + 1
+    uint32_t span;     // hi(dec(15 - A)) - hi(dec(-A)) - 1 (0 if negative)
+    uint32_t hk;       // hi(p) - (1076 << 20)
+    uint32_t plo;      // lo(p)
+    uint32_t lim;      // 32-bit delta bound: |v| high word below it -> |v * 10^A| < 2^30
+    uint32_t pad;
+};
+struct cert_row32 {
+    float p;
+    uint32_t lo;       // bits(dec(-A))
+    uint32_t span;     // bits(dec(6 - A)) - bits(dec(-A))
+    uint32_t hk;       // bits(p) - (151 << 23)
+};
+#ifdef FB200_KERNEL_TU
+FB_TABLE_SPACE cert_row64 g_cert_f64[23];
+FB_TABLE_SPACE cert_row32 g_cert_f32[11];
+#endif
+
 // Device error word: ((key) << 8) | code, lowest key wins (atomicMin).
 enum : uint32_t {
     DEV_OK = 0,
@@ -205,6 +228,16 @@ __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
 }
 __device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// relaxed 32-bit load/store without a compiler memory clobber (self-contained words: the
+// encoder's look-ahead sample verdicts, see encode.cu)
+__device__ __forceinline__ uint32_t ld_relaxed32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_relaxed32(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v));
 }
 __device__ __forceinline__ uint32_t ld_acquire32(const uint32_t* p) {
     uint32_t v;

@@ -21,6 +21,7 @@ struct encode_ws {
     uint32_t* sizes;              // [n_chunks] encoded chunk sizes
     uint64_t* tile_status;        // [n_tiles] placement look-back words
     uint64_t* batch_prefix;       // [n_batches] payload prefix of each batch | ready bit
+    uint32_t* look;               // [n_chunks] sample verdicts (sample_chunks_kernel)
     uint32_t* ticket;             // placement tile ticket counter
     unsigned long long* error;    // (chunk << 8 | code), ~0 = none
     uint64_t* total;              // archive bytes, written by the placement kernel

@@ -41,7 +41,32 @@ cudaError_t upload_tables() {
         const float v = std::strtof(buf, nullptr);
         std::memcpy(&dec32[k + 38], &v, 4);
     }
+    // certification parameters per candidate scale (dpds.cuh cert_params_for)
+    cert_row64 c64[23];
+    cert_row32 c32[11];
+    for (int a = 0; a < 23; ++a) {
+        uint64_t pb;
+        std::memcpy(&pb, &p64[a], 8);
+        const uint32_t L = (uint32_t)(dec64[308 - a] >> 32), U = (uint32_t)(dec64[308 + 15 - a] >> 32);
+        c64[a].p = p64[a];
+        c64[a].lo1 = L + 1u;
+        c64[a].span = U > L + 1u ? U - L - 1u : 0u;
+        c64[a].hk = (uint32_t)(pb >> 32) - (1076u << 20);
+        c64[a].plo = (uint32_t)pb;
+        c64[a].lim = (2074u - ((uint32_t)(pb >> 32) >> 20)) << 20;
+        c64[a].pad = 0;
+    }
+    for (int a = 0; a < 11; ++a) {
+        uint32_t pb;
+        std::memcpy(&pb, &p32[a], 4);
+        c32[a].p = p32[a];
+        c32[a].lo = dec32[38 - a];
+        c32[a].span = dec32[38 + 6 - a] - dec32[38 - a];
+        c32[a].hk = pb - (151u << 23);
+    }
     cudaError_t e;
+    if ((e = cudaMemcpyToSymbol(g_cert_f64, c64, sizeof c64))) return e;
+    if ((e = cudaMemcpyToSymbol(g_cert_f32, c32, sizeof c32))) return e;
     if ((e = cudaMemcpyToSymbol(g_pow10_f64, p64, sizeof p64))) return e;
     if ((e = cudaMemcpyToSymbol(g_pow10_f32, p32, sizeof p32))) return e;
     if ((e = cudaMemcpyToSymbol(g_rpow10_f64, r64, sizeof r64))) return e;
