@@ -168,13 +168,21 @@ constexpr int encode_min_blocks() {
 // ~250 warp-instructions per sample step, so the sampler is issue-bound: 8 samples per
 // chunk (4 chunks per warp) instead of the 32 of the in-kernel phase it replaces (cfg2
 // sampler 78 us at 32 samples per chunk).
-constexpr int kSamples = 8;
+#ifndef FB_SAMPLES
+#define FB_SAMPLES 8
+#endif
+constexpr int kSamples = FB_SAMPLES;
+#ifndef FB_ENC_PDL
+#define FB_ENC_PDL 1
+#endif
+constexpr bool kEncPDL = FB_ENC_PDL != 0;
 template <typename T>
 __global__ void __launch_bounds__(256) sample_chunks_kernel(const T* __restrict__ in, geometry g,
                                                             uint32_t* __restrict__ look) {
     constexpr int CPW = 32 / kSamples;   // chunks per warp
     const int lane = threadIdx.x & 31;
     const uint64_t c = ((uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * CPW + (uint64_t)(lane / kSamples);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the encode launch may start
     const uint32_t n = g.chunk_n;
     const uint32_t i = (uint32_t)(lane % kSamples) % n;
     T v = T(0);
@@ -251,10 +259,6 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     const uint32_t c = b * g.cpb + ci;                      // < 2^31 chunks per launch
     const uint64_t v0 = (uint64_t)b * g.batch_values + (uint64_t)ci * n;
     const bool active = tid < NC;
-
-    // ---- phase 1 (sample_chunks_kernel): this chunk's sample verdict, loaded beside the
-    //      values (f32: after them -- the 32-register budget spilled with it early) ----
-    uint32_t F = sizeof(T) == 8 ? __ldg(ws.look + c) : 0u;
 
     // The chunk L.pf_ahead CTAs later (about one generation of resident CTAs) is pulled into
     // L2 with one bulk prefetch, so its CTA's value loads hit L2 instead of waiting on DRAM
@@ -338,9 +342,12 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     }
 
     // ---- analyze, phase 1 (decided ahead by sample_chunks_kernel): A0 = the largest
-    //      alpha of 32 sampled chunk values, attained, so alpha_max >= A0; bit 31 = a
-    //      sampled exception (the chunk is Case 2, phase 2 is skipped) ----
-    if (sizeof(T) == 4) F = __ldg(ws.look + c);
+    //      alpha of kSamples sampled chunk values, attained, so alpha_max >= A0; bit 31 =
+    //      a sampled exception (the chunk is Case 2, phase 2 is skipped).  The first encode
+    //      launch starts beside the sampler (programmatic dependent launch): the value
+    //      loads above are in flight while it waits for the sampler's results. ----
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    uint32_t F = __ldg(ws.look + c);
     const int A0 = (F & 0x7fffffffu) ? 31 - __clz((int)(F & 0x7fffffffu)) : 0;
 
     // ---- analyze, phase 2: lean certification of every value at A0 (dpds.cuh); the
@@ -1125,8 +1132,19 @@ cudaError_t launch_encode(const T* d_in, const geometry& g, uint8_t* d_out, uint
             e = launch_place_final(threads, L.place_tiles, g, d_out, out_cap, ws, L, hdr, st);
         } else {
             const unsigned gx = (unsigned)(g.cpb > L.place_tiles ? g.cpb : L.place_tiles);
-            kern<<<dim3(gx, (unsigned)(1 + nb)), threads, smem, st>>>(d_in, g, d_out, out_cap, ws, L, hdr);
-            e = cudaGetLastError();
+            // the first launch overlaps the sampler's tail (programmatic dependent launch;
+            // its CTAs wait for the sampler after issuing their value loads)
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(gx, (unsigned)(1 + nb));
+            cfg.blockDim = dim3(threads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = (k == 0 && kEncPDL) ? 1 : 0;
+            e = cudaLaunchKernelEx(&cfg, kern, d_in, g, d_out, out_cap, ws, L, hdr);
         }
         if (e) return e;
         placed = placeable;
