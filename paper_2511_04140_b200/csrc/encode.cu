@@ -21,7 +21,7 @@
 //            (bitplane.hpp:113-122, chunk_codec.hpp:59-73)
 //   emit     every thread writes its column of every row into the smem image (sparse
 //            rows: bitmap bytes + payload at warp prefix + ballot rank,
-//            bitplane.hpp:126-148); 16-B stores into the chunk's scratch slot
+//            bitplane.hpp:126-148); one TMA bulk copy into the chunk's scratch slot
 //
 // placement (place_tile: grid row 0 of a later wave's encode launch, and
 // place_final_kernel after the last wave): scan of the chunk sizes in tiles with a
@@ -144,16 +144,23 @@ __device__ __forceinline__ uint32_t nonzero_bytes(uint32_t w) {
 // resident CTAs of <= 128 threads per SM the register budget targets.  The encoder is
 // latency-bound between its block barriers, so occupancy pays until spills dominate:
 // f64 at 9 (56 registers, no spills; cfg2 encode 1.139 ms at 8 blocks, 1.106 ms at 9,
-// 1.143 ms at 10 with spills), f32 at 16 (32 registers; cfg3 encode 1.65 ms at 8 blocks,
-// 1.39 ms at 12, 1.35 ms at 16)
+// 1.143 ms at 10 with spills; re-checked with phase 1 in the sampler: compress 1.134 ms at
+// 8, 1.126 ms at 9), f32 at 12 (cfg3 encode 1.65 ms at 8 blocks, 1.39 ms at 12, 1.35 ms
+// at 16 with the in-kernel phase 1; without it: compress 1.508 ms at 12, 1.542 ms at 14
+// and 16 -- 32 registers spilled)
 #ifndef FB_ENC_MIN_BLOCKS
 #define FB_ENC_MIN_BLOCKS 9
+#endif
+// image store by one TMA bulk copy (cfg2 compress 1.125 -> 1.115 ms, cfg3 1.508 -> 1.465
+// ms against the 16-B vector store loop over all threads)
+#ifndef FB_ENC_BULK_STORE
+#define FB_ENC_BULK_STORE 1
 #endif
 #ifndef FB_ENC_VEC_LOADS
 #define FB_ENC_VEC_LOADS 1
 #endif
 #ifndef FB_ENC_MIN_BLOCKS32
-#define FB_ENC_MIN_BLOCKS32 16
+#define FB_ENC_MIN_BLOCKS32 12
 #endif
 template <typename T, int NT>
 constexpr int encode_min_blocks() {
@@ -700,7 +707,20 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     uint4* dst = reinterpret_cast<uint4*>(ws.images + slot * (uint64_t)ws.slot);
     const uint4* srcv = reinterpret_cast<const uint4*>(s_stage);
     const uint32_t nvec = (size + 15) >> 4;
+#if FB_ENC_BULK_STORE
+    // one TMA bulk copy smem -> global (the image's generic-proxy smem writes are made
+    // visible to the async proxy first); the issuing thread keeps the CTA (and its smem)
+    // alive until the copy has read the staging buffer
+    if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                     "r"((uint32_t)__cvta_generic_to_shared(srcv)), "r"(nvec * 16u) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+#else
     for (uint32_t vv = tid; vv < nvec; vv += NT) dst[vv] = srcv[vv];
+#endif
 }
 
 // Placement: chunk images -> archive.  A tile of NT consecutive chunks per CTA (grid row 0
