@@ -441,13 +441,14 @@ def run_ours(args, rank, world, local_rank):
             traffic = None
     roofline = {"bound": "hbm", "achieved": algo / dom_t / 1e9, "peak": peak, "unit": "GB/s",
                 "frac": algo / dom_t / 1e9 / peak, "traffic": traffic,
-                "kernel": "encode_chunks_kernel (+ fused placement)" if dom == "encode" else "decode_chunks_kernel",
+                "kernel": "encode_chunks_kernel (+ sampler, placement)" if dom == "encode" else "decode_chunks_kernel",
                 "peak_source": peak_src,
                 "per_launch_bytes": algo,
                 "compress_ms": 1e3 * enc_avg, "decompress_ms": 1e3 * dec_avg,
                 "compress_frac": algo / enc_avg / 1e9 / peak, "decompress_frac": algo / dec_avg / 1e9 / peak,
-                "note": "compress = every encode launch incl. the fused placement and the final "
-                        "placement launch; decompress = frame walker + decoder"}
+                "note": "compress = the chunk sampler (phase 1) + every encode launch incl. the fused "
+                        "placement + the final placement launch; decompress = frame walker + decoder; "
+                        "traffic = DRAM bytes of the dominant codec kernel alone (ncu --set full)"}
     cpu = None
     if world == 1 and not args.no_cpu and host_vals is not None:
         sample_n = min(n, args.cpu_max_values)

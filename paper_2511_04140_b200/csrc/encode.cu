@@ -945,12 +945,19 @@ __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_
 // Two shapes: NTHR = NT for large calls (cfg2/cfg3 compress -1.2 % / -2.8 % against the
 // wide shape), NTHR = 4 NT (capped at 1024) when there are fewer tiles than two per SM,
 // where the copy is latency-bound (cfg1 compress 0.057 -> 0.034 ms).
+#ifndef FB_PLACE_MINB
+#define FB_PLACE_MINB 1
+#endif
+#ifndef FB_PLACE_U
+#define FB_PLACE_U 4
+#endif
 template <int NT, int NTHR>
-__global__ void __launch_bounds__(NTHR) place_final_kernel(geometry g, uint8_t* __restrict__ out, uint64_t out_cap,
-                                                           encode_ws ws, encode_launch L, archive_header_bytes hdr) {
+__global__ void __launch_bounds__(NTHR, NTHR == NT ? FB_PLACE_MINB : 1)
+    place_final_kernel(geometry g, uint8_t* __restrict__ out, uint64_t out_cap, encode_ws ws, encode_launch L,
+                       archive_header_bytes hdr) {
     extern __shared__ __align__(16) uint8_t smem[];
     // the wide shape keeps 8 vectors per lane in flight (few CTAs: latency-bound)
-    place_tile<NT, NTHR == NT ? 4 : 8, NTHR>(g, out, out_cap, ws, L, hdr, smem);
+    place_tile<NT, NTHR == NT ? FB_PLACE_U : 8, NTHR>(g, out, out_cap, ws, L, hdr, smem);
 }
 
 // one thread per byte column, rounded to an instantiated CTA size

@@ -52,7 +52,7 @@ for f in ["bench_full.log", f"bench_{W}.log"]:
         break
 rows = []
 traffic = {}
-for k in ["encode_chunks_kernel", "decode_chunks_kernel"]:
+for k in ["encode_chunks_kernel", "decode_chunks_kernel", "sample_chunks_kernel"]:
     rep = os.path.join(src, f"prof_{W}_{k}.ncu-rep")
     if not os.path.exists(rep):
         continue
