@@ -561,55 +561,52 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
     for (int i = 0; i < nwarps; ++i) w = (int)s_warpw[i] > w ? (int)s_warpw[i] : w;
     const int fb = (w + 7) >> 3;
 
-    // ---- sizes and row offsets (warp 0): plane p is row w-1-p ----
+    // ---- sizes and row offsets (warp 0): plane p is row w-1-p.  Lane L sizes plane L;
+    //      planes 32..63 (f64 chunks with w > 32 only) go first, their total offsets the
+    //      lower rows.  (f32 and the common w <= 32 skip that half: cfg2 w is ~14-20.) ----
     if (warp == 0) {
-        uint32_t nz0 = 0, nz1 = 0;  // nonzero bytes of planes `lane` and `lane + 32`
-        uint32_t wp0[nwarps], wp1[nwarps];  // payload bytes of planes lane / lane+32 in warps before q
-#pragma unroll
-        for (int q = 0; q < nwarps; ++q) {
-            const int wq = (int)s_warpw[q];
-            const uint32_t c0 = lane < wq ? (s_nzc[q][lane >> 2] >> (8 * (lane & 3))) & 0xffu : 0u;
-            const uint32_t c1 = lane + 32 < wq ? (s_nzc[q][(lane + 32) >> 2] >> (8 * (lane & 3))) & 0xffu : 0u;
-            wp0[q] = nz0;
-            wp1[q] = nz1;
-            nz0 += c0;
-            nz1 += c1;
-        }
         auto row_cost = [&](int p, uint32_t nz, bool& dns) -> uint32_t {
             dns = false;
             if (p >= w) return 0;
             dns = (uint32_t)NC - nz <= (uint32_t)BM;        // bitplane.hpp:113-115
             return dns ? (uint32_t)NC : (uint32_t)BM + nz;  // bitplane.hpp:117-122
         };
-        bool d0, d1;
-        const uint32_t c0 = row_cost(lane, nz0, d0);
-        const uint32_t c1 = row_cost(lane + 32, nz1, d1);
-        // rows are emitted from the highest plane down: offset(p) = sum of cost(p' > p)
-        uint32_t s1 = c1, s0 = c0;
+        // plane p of the half starting at P0: row cost, reverse (suffix) scan, row offset,
+        // per-warp sparse payload starts; returns the half's total cost
+        auto size_half = [&](const int P0, const uint32_t above, bool& dns) -> uint32_t {
+            const int p = P0 + lane;
+            uint32_t nz = 0;
+            uint32_t wp[nwarps];  // payload bytes of plane p in the warps before q
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t t1 = __shfl_down_sync(0xffffffffu, s1, d);
-            const uint32_t t0 = __shfl_down_sync(0xffffffffu, s0, d);
-            if (lane + d < 32) {
-                s1 += t1;
-                s0 += t0;
+            for (int q = 0; q < nwarps; ++q) {
+                const uint32_t cq = p < (int)s_warpw[q] ? (s_nzc[q][p >> 2] >> (8 * (lane & 3))) & 0xffu : 0u;
+                wp[q] = nz;
+                nz += cq;
             }
-        }
-        const uint32_t tot1 = __shfl_sync(0xffffffffu, s1, 0);
-        const uint32_t tot0 = __shfl_sync(0xffffffffu, s0, 0);
-        const uint32_t base = HDR + fb;
-        const uint32_t ro1 = base + (s1 - c1), ro0 = base + tot1 + (s0 - c0);
-        s_rowoff[lane + 32] = ro1;
-        s_rowoff[lane] = ro0;
-        // sparse payload start of plane p for warp q: row offset + bitmap + earlier warps
+            const uint32_t cost = row_cost(p, nz, dns);
+            // rows are emitted from the highest plane down: offset(p) = sum of cost(p' > p)
+            uint32_t sfx = cost;
 #pragma unroll
-        for (int q = 0; q < nwarps; ++q) {
-            s_pbase[q * 64 + lane] = ro0 + (uint32_t)BM + wp0[q];
-            s_pbase[q * 64 + lane + 32] = ro1 + (uint32_t)BM + wp1[q];
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t t = __shfl_down_sync(0xffffffffu, sfx, d);
+                if (lane + d < 32) sfx += t;
+            }
+            const uint32_t ro = HDR + fb + above + (sfx - cost);
+            s_rowoff[p] = ro;
+#pragma unroll
+            for (int q = 0; q < nwarps; ++q) s_pbase[q * 64 + p] = ro + (uint32_t)BM + wp[q];
+            return __shfl_sync(0xffffffffu, sfx, 0);
+        };
+        uint32_t tot1 = 0, dm1 = 0;
+        if (tr::width > 32 && w > 32) {
+            bool d1;
+            tot1 = size_half(32, 0u, d1);
+            dm1 = __ballot_sync(0xffffffffu, d1);
         }
+        bool d0;
+        const uint32_t tot0 = size_half(0, tot1, d0);
         const uint32_t dm0 = __ballot_sync(0xffffffffu, d0);
-        const uint32_t dm1 = __ballot_sync(0xffffffffu, d1);
-        const uint32_t size = w ? base + tot1 + tot0 : (uint32_t)HDR;
+        const uint32_t size = w ? HDR + fb + tot1 + tot0 : (uint32_t)HDR;
         if (lane == 0) {
             s_dense = ((uint64_t)dm1 << 32) | dm0;
             s_size = size;

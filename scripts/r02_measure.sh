@@ -14,5 +14,9 @@ done
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:encode_chunks_kernel -s 2 -c 1 -o gpurun_out/prof_cfg3_encode_chunks_kernel -f \
   python bench.py --workload cfg3 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_full_cfg3.log 2>&1; echo "ncu cfg3=$?"
 python scripts/save_profile.py $TAG cfg2 > gpurun_out/save_profile.log 2>&1; echo "save=$?"
+# the merge back is capped at 64 MiB: keep only the cfg2 encoder report (source view)
+python scripts/ncu_regions.py gpurun_out/prof_cfg3_encode_chunks_kernel.ncu-rep > gpurun_out/cfg3_encode_regions.txt 2>&1
+python scripts/ncu_lines2.py gpurun_out/prof_cfg2_decode_chunks_kernel.ncu-rep 0.5 > gpurun_out/cfg2_decode_lines.txt 2>&1
+rm -f gpurun_out/prof_cfg2_decode_chunks_kernel.ncu-rep gpurun_out/prof_cfg2_sample_chunks_kernel.ncu-rep gpurun_out/prof_cfg3_encode_chunks_kernel.ncu-rep
 bash scripts/r02_full.sh
 mkdir -p gpurun_out/profiles_$TAG && cp -r profiles/$TAG/. gpurun_out/profiles_$TAG/ && cp profiles/ncu_traffic.json gpurun_out/profiles_$TAG/

@@ -213,3 +213,40 @@ def test_inputs_at_every_16_byte_phase(codec, oracle, prec, shift):
     arc, nb = codec.compress_device(d, chunk_n=N, batch_values=N * 8)
     assert arc[:nb].cpu().numpy().tobytes() == want
     assert torch.equal(codec.decompress_device(arc, nb).cpu(), d.cpu())
+
+
+# ---- phase 1 runs in sample_chunks_kernel on each chunk's first 8 values (encode.cu) ----
+@pytest.mark.parametrize("prec", [F64, F32])
+@pytest.mark.parametrize("where", ["sampled", "unsampled"])
+def test_exception_inside_and_outside_the_sample_window(codec, oracle, prec, where):
+    dt = np.float64 if prec == F64 else np.float32
+    rng = np.random.default_rng(21)
+    base = decimals(rng, 16 * N, 2, -1e3, 1e3, dt)
+    specials = np.array([np.nan, -np.inf, -0.0, 1e-310 if prec == F64 else 1e-40], dt)
+
+    def inject(c, r):
+        i = int(r.integers(0, 8)) if where == "sampled" else int(r.integers(8, len(c)))
+        c[min(i, len(c) - 1)] = specials[int(r.integers(0, len(specials)))]
+    check(codec, oracle, chunks_with(rng, base, inject))
+
+
+@pytest.mark.parametrize("prec", [F64, F32])
+@pytest.mark.parametrize("sample_dp,rest_dp", [(0, 3), (4, 1), (2, 2)])
+def test_sample_window_coarser_or_finer_than_the_chunk(codec, oracle, prec, sample_dp, rest_dp):
+    # coarser sample: alpha_max > A0 (general Case-1 path); finer: every value certified at A0
+    dt = np.float64 if prec == F64 else np.float32
+    rng = np.random.default_rng(22 + sample_dp)
+    v = decimals(rng, 12 * N, rest_dp, -900, 900, dt)
+    s = decimals(rng, 12 * N, sample_dp, -900, 900, dt)
+    for c0 in range(0, len(v), N):
+        v[c0:c0 + 8] = s[c0:c0 + 8]
+    check(codec, oracle, v)
+
+
+@pytest.mark.parametrize("prec", [F64, F32])
+@pytest.mark.parametrize("tail", [1, 3, 7, 8, 9])
+def test_final_chunk_shorter_than_the_sample(codec, oracle, prec, tail):
+    # the sampler reads +0.0 padding past a short final chunk (pipeline.hpp:205-215)
+    dt = np.float64 if prec == F64 else np.float32
+    rng = np.random.default_rng(30 + tail)
+    check(codec, oracle, decimals(rng, 5 * N + tail, 3, -50, 50, dt), bv=N * 2)
