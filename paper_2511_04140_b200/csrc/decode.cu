@@ -563,6 +563,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_suspend(bar, parity)) {
     }
 }
+#ifndef FB_DEC_CONS_SLEEP
+#define FB_DEC_CONS_SLEEP 0
+#endif
+// consumer-side wait: a failed try_wait backs off for FB_DEC_CONS_SLEEP ns (A/B knob)
+__device__ __forceinline__ void mbar_wait_cons(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_suspend(bar, parity)) {
+        if (FB_DEC_CONS_SLEEP) __nanosleep(FB_DEC_CONS_SLEEP);
+    }
+}
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
 }
@@ -933,7 +942,7 @@ __global__ void __launch_bounds__(NT + 32 * decode_cfg<T>::producers, decode_min
         const uint32_t pw = it % kProducers;
         if ((exited >> pw) & 1u) continue;
         const int sl = (int)(it % kDecodeSlots);
-        mbar_wait(&s_full[sl], (it / kDecodeSlots) & 1);
+        mbar_wait_cons(&s_full[sl], (it / kDecodeSlots) & 1);
         SI& si = s_info[sl];
         const uint32_t kind = si.kind;
         if (kind == SLOT_EXIT) {
