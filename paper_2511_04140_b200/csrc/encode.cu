@@ -153,6 +153,12 @@ __device__ __forceinline__ uint32_t nonzero_bytes(uint32_t w) {
 #endif
 // image store by one TMA bulk copy (cfg2 compress 1.125 -> 1.115 ms, cfg3 1.508 -> 1.465
 // ms against the 16-B vector store loop over all threads)
+#ifndef FB_ENC_SEL_TREE
+#define FB_ENC_SEL_TREE 0
+#endif
+#ifndef FB_SAMPLE_K64
+#define FB_SAMPLE_K64 3
+#endif
 #ifndef FB_ENC_BULK_STORE
 #define FB_ENC_BULK_STORE 1
 #endif
@@ -201,7 +207,7 @@ __global__ void __launch_bounds__(256) sample_chunks_kernel(const T* __restrict_
         // values past a short final chunk are its +0.0 padding (pipeline.hpp:205-215)
         if (i < len) v = __ldg(in + b * g.batch_values + ci * n + i);
     }
-    const int a = dp_alpha_k<T, sizeof(T) == 8 ? 4 : 3>(v);
+    const int a = dp_alpha_k<T, sizeof(T) == 8 ? FB_SAMPLE_K64 : 3>(v);
     uint32_t f = a < 0 ? 0x80000000u : (1u << a);
 #pragma unroll
     for (int d = 1; d < kSamples; d <<= 1) f |= __shfl_xor_sync(0xffffffffu, f, d);
@@ -682,9 +688,18 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
             }
             {
                 const int kl = lane >> 2, ql = lane & 3;
+#if FB_ENC_SEL_TREE
+                // mk[kl] by a 3-level select tree on the bits of kl (7 selects, 3 tests)
+                const bool k1 = kl & 1, k2 = kl & 2, k4 = kl & 4;
+                const uint32_t m01 = k1 ? mk[1] : mk[0], m23 = k1 ? mk[3] : mk[2];
+                const uint32_t m45 = k1 ? mk[5] : mk[4], m67 = k1 ? mk[7] : mk[6];
+                const uint32_t m03 = k2 ? m23 : m01, m47 = k2 ? m67 : m45;
+                const uint32_t mm = k4 ? m47 : m03;
+#else
                 uint32_t mm = mk[0];
 #pragma unroll
                 for (int k = 1; k < 8; ++k) mm = kl == k ? mk[k] : mm;
+#endif
                 const uint32_t bm = __brev(mm >> (8 * ql)) >> 24;
                 if (((sblk >> kl) & 1u) && 4 * warp + ql < BM) s_stage[s_rowoff[8 * sb + kl] + 4 * warp + ql] = (uint8_t)bm;
             }
@@ -948,13 +963,18 @@ __device__ void place_tile(const geometry& g, uint8_t* __restrict__ out, uint64_
 #ifndef FB_PLACE_U
 #define FB_PLACE_U 4
 #endif
-template <int NT, int NTHR>
+#ifndef FB_PLACE_U32
+#define FB_PLACE_U32 2
+#endif
+// U: vectors per lane in flight in the NT shape -- 4 for f64 images, 2 for the smaller
+// f32 ones (cfg3 compress 1.426 -> 1.416 ms; cfg2 loses 1.8 % at 2, 5.7 % at 8)
+template <int NT, int NTHR, int U>
 __global__ void __launch_bounds__(NTHR, NTHR == NT ? FB_PLACE_MINB : 1)
     place_final_kernel(geometry g, uint8_t* __restrict__ out, uint64_t out_cap, encode_ws ws, encode_launch L,
                        archive_header_bytes hdr) {
     extern __shared__ __align__(16) uint8_t smem[];
     // the wide shape keeps 8 vectors per lane in flight (few CTAs: latency-bound)
-    place_tile<NT, NTHR == NT ? FB_PLACE_U : 8, NTHR>(g, out, out_cap, ws, L, hdr, smem);
+    place_tile<NT, NTHR == NT ? U : 8, NTHR>(g, out, out_cap, ws, L, hdr, smem);
 }
 
 // one thread per byte column, rounded to an instantiated CTA size
@@ -1062,7 +1082,7 @@ encode_ws carve_encode_ws(void* scratch, const geometry& g, uint32_t* ticket, un
     return ws;
 }
 
-static cudaError_t launch_place_final(uint32_t threads, uint32_t tiles, const geometry& g, uint8_t* d_out,
+static cudaError_t launch_place_final(bool f32, uint32_t threads, uint32_t tiles, const geometry& g, uint8_t* d_out,
                                       uint64_t out_cap, const encode_ws& ws, const encode_launch& L,
                                       const archive_header_bytes& hdr, cudaStream_t st) {
     // FALCON_PLACE_WIDE_BELOW (tiles) overrides the shape choice (tests force both shapes)
@@ -1079,8 +1099,9 @@ static cudaError_t launch_place_final(uint32_t threads, uint32_t tiles, const ge
     switch (threads) {
 #define FB_PLACE(n)                                                                                          \
     case n:                                                                                                  \
-        if (wide) place_final_kernel<n, (4 * n <= 1024 ? 4 * n : 1024)><<<tiles, nthr, smem, st>>>(g, d_out, out_cap, ws, L, hdr); \
-        else place_final_kernel<n, n><<<tiles, nthr, smem, st>>>(g, d_out, out_cap, ws, L, hdr);           \
+        if (wide) place_final_kernel<n, (4 * n <= 1024 ? 4 * n : 1024), 8><<<tiles, nthr, smem, st>>>(g, d_out, out_cap, ws, L, hdr); \
+        else if (f32) place_final_kernel<n, n, FB_PLACE_U32><<<tiles, nthr, smem, st>>>(g, d_out, out_cap, ws, L, hdr); \
+        else place_final_kernel<n, n, FB_PLACE_U><<<tiles, nthr, smem, st>>>(g, d_out, out_cap, ws, L, hdr); \
         break;
     FB_PLACE(32) FB_PLACE(64) FB_PLACE(96) FB_PLACE(128) FB_PLACE(160) FB_PLACE(192) FB_PLACE(224)
     FB_PLACE(256) FB_PLACE(512)
@@ -1153,7 +1174,7 @@ cudaError_t launch_encode(const T* d_in, const geometry& g, uint8_t* d_out, uint
         L.pf_ahead = pf;
         if (nb == 0 && L.place_tiles == 0) continue;
         if (nb == 0) {
-            e = launch_place_final(threads, L.place_tiles, g, d_out, out_cap, ws, L, hdr, st);
+            e = launch_place_final(sizeof(T) == 4, threads, L.place_tiles, g, d_out, out_cap, ws, L, hdr, st);
         } else {
             const unsigned gx = (unsigned)(g.cpb > L.place_tiles ? g.cpb : L.place_tiles);
             // the first launch overlaps the sampler's tail (programmatic dependent launch;
