@@ -124,8 +124,8 @@ __device__ __forceinline__ bool near_integer(T s, T* N) {
 // K consecutive candidate scales are tested per step (independent multiply/round
 // chains: one step costs the latency of one candidate); the first candidate passing
 // the gap test decides, exactly as in the sequential loop.  K = 1 keeps the call-site
-// footprint small for the encoder's rare per-thread fallback; K = 4 is the latency-
-// bound sampling of phase 1.
+// footprint small for the encoder's rare per-thread fallback; K = 3 is phase 1's
+// sampling (sample_chunks_kernel, encode.cu).
 template <typename T, int K>
 __device__ __forceinline__ int dp_alpha_k(T v) {
     using X = fpx<T>;

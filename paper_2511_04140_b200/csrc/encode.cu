@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(NT, encode_min_blocks<T, NT>())
 
     // The chunk L.pf_ahead CTAs later (about one generation of resident CTAs) is pulled into
     // L2 with one bulk prefetch, so its CTA's value loads hit L2 instead of waiting on DRAM
-    // (the load latency sits on every CTA's critical path: phase 1 cannot start without it).
+    // (the load latency sits on every CTA's critical path: phase 2 cannot start without it).
 #ifndef FB_ENC_NO_PREFETCH
     // (f64 only: cfg2 compress -1.2 %; f32 had no gain and its 32-register budget spilled)
     if (sizeof(T) == 8 && tid == 0 && L.pf_ahead) {
